@@ -1,0 +1,416 @@
+/*
+ * oracle/oracle.c -- plain, slow, fp64 CPU oracle for the FHR hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with the CUDA path
+ * (paper_2410_22500_b200/csrc); neither side includes or links the other.
+ *
+ * Every function follows a passage of /root/reference/PAPER.md (cited as
+ * PAPER.md:<line>, with the equation/algorithm it falls in) or, where the
+ * paper is silent, a reading listed in DESIGN.md §3 ("Readings").  All
+ * arithmetic is IEEE fp64 in the order the formula states; OpenMP is used
+ * only across independent outputs, each of which is accumulated in a fixed
+ * sequential order, so results do not depend on the thread count.
+ *
+ * Notation (§II): N_v views, N_r detector rows (slices),
+ * N_c detector columns (image width), N_k wavelength bins, N_p = N_v N_r N_c,
+ * N_x = N_r N_c N_c.  The projection matrix p in R^{N_p x N_k}
+ * is stored row-major with row index p = (v*N_r + r)*N_c + c and the bin
+ * index fastest ("y_{v,r,c,k}").  The subspace dimension N_s
+ * is called K here; D is stored as (D^s)^T, K x N_k.
+ *
+ * Parity pins: see tests/test_oracle_*.py.  Nothing in this file is
+ * "parity unpinned".
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_PI 3.14159265358979323846264338327950288
+
+static void set_threads(int nthreads) {
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* ------------------------------------------------------------------------ */
+/* Subspace extraction: Eq. 4                            */
+/*   (V^s, D^s) = argmin_{V>=0, D>=0} || p - V D^T ||_F^2                    */
+/* solved (reading R1, R2, R3 in DESIGN.md) by the textbook Lee-Seung        */
+/* Frobenius multiplicative updates, V half-step first, denominators         */
+/* floored at 1e-30, on Y+ = max(Y, 0) (reading R6).                         */
+/* ------------------------------------------------------------------------ */
+
+static inline double yplus(const float* Y, int64_t ld, int64_t p, int64_t l) {
+    double y = (double)Y[p * ld + l];
+    return y > 0.0 ? y : 0.0;
+}
+
+/* || Y+ - V D ||_F^2, straight from the definition. */
+double oracle_nmf_objective(const float* Y, int64_t Np, int64_t Nk, int64_t ld_y, int K,
+                            const double* V, const double* D, int nthreads) {
+    set_threads(nthreads);
+    double* rows = (double*)malloc(sizeof(double) * (size_t)(Np > 0 ? Np : 1));
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < Np; ++p) {
+        double s = 0.0;
+        for (int64_t l = 0; l < Nk; ++l) {
+            double vd = 0.0;
+            for (int k = 0; k < K; ++k) vd += V[p * K + k] * D[(int64_t)k * Nk + l];
+            double e = yplus(Y, ld_y, p, l) - vd;
+            s += e * e;
+        }
+        rows[p] = s;
+    }
+    double f = 0.0;
+    for (int64_t p = 0; p < Np; ++p) f += rows[p];
+    free(rows);
+    return f;
+}
+
+/*
+ * n_iter Lee-Seung iterations from the caller's (V, D) (in/out, fp64).
+ * One iteration (reading R2, V first):
+ *   A = Y+ D^T;  G = D D^T;  V <- V .* A ./ max(V G, 1e-30)
+ *   B = V^T Y+;  H = V^T V;  D <- D .* B ./ max(H D, 1e-30)
+ * obj (nullable, 2*n_iter): ||Y+ - V D||^2 after the V half and after the D
+ * half of every iteration, by oracle_nmf_objective.
+ */
+int oracle_nmf(const float* Y, int64_t Np, int64_t Nk, int64_t ld_y, int K,
+               double* V, double* D, int n_iter, double* obj, int nthreads) {
+    if (Np < 0 || Nk < 0 || K < 1 || K > 16 || ld_y < Nk || n_iter < 0) return 1;
+    set_threads(nthreads);
+    double* G = (double*)malloc(sizeof(double) * K * K);
+    double* H = (double*)malloc(sizeof(double) * K * K);
+    double* B = (double*)malloc(sizeof(double) * (size_t)K * (size_t)(Nk > 0 ? Nk : 1));
+    for (int it = 0; it < n_iter; ++it) {
+        /* G = D D^T */
+        for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) {
+                double s = 0.0;
+                for (int64_t l = 0; l < Nk; ++l) s += D[(int64_t)a * Nk + l] * D[(int64_t)b * Nk + l];
+                G[a * K + b] = s;
+            }
+        /* V half-step: rows are independent. */
+#pragma omp parallel for schedule(static)
+        for (int64_t p = 0; p < Np; ++p) {
+            double A[64], VG[64];
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int64_t l = 0; l < Nk; ++l) s += yplus(Y, ld_y, p, l) * D[(int64_t)k * Nk + l];
+                A[k] = s;
+            }
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int j = 0; j < K; ++j) s += V[p * K + j] * G[j * K + k];
+                VG[k] = s;
+            }
+            for (int k = 0; k < K; ++k) {
+                double den = VG[k] > 1e-30 ? VG[k] : 1e-30;
+                V[p * K + k] = V[p * K + k] * A[k] / den;
+            }
+        }
+        if (obj) obj[2 * it] = oracle_nmf_objective(Y, Np, Nk, ld_y, K, V, D, nthreads);
+        /* H = V^T V (fixed row order). */
+        for (int a = 0; a < K; ++a)
+            for (int b = 0; b < K; ++b) {
+                double s = 0.0;
+                for (int64_t p = 0; p < Np; ++p) s += V[p * K + a] * V[p * K + b];
+                H[a * K + b] = s;
+            }
+        /* B = V^T Y+: every (k, l) output sums rows in order p = 0..Np-1. */
+#pragma omp parallel for schedule(static)
+        for (int64_t l0 = 0; l0 < Nk; l0 += 64) {
+            int64_t l1 = l0 + 64 < Nk ? l0 + 64 : Nk;
+            double acc[16 * 64];
+            for (int k = 0; k < K; ++k)
+                for (int64_t l = l0; l < l1; ++l) acc[k * 64 + (l - l0)] = 0.0;
+            for (int64_t p = 0; p < Np; ++p)
+                for (int64_t l = l0; l < l1; ++l) {
+                    double y = yplus(Y, ld_y, p, l);
+                    for (int k = 0; k < K; ++k) acc[k * 64 + (l - l0)] += V[p * K + k] * y;
+                }
+            for (int k = 0; k < K; ++k)
+                for (int64_t l = l0; l < l1; ++l) B[(int64_t)k * Nk + l] = acc[k * 64 + (l - l0)];
+        }
+        /* D half-step: columns are independent. */
+        for (int64_t l = 0; l < Nk; ++l) {
+            double HD[64];
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int j = 0; j < K; ++j) s += H[k * K + j] * D[(int64_t)j * Nk + l];
+                HD[k] = s;
+            }
+            for (int k = 0; k < K; ++k) {
+                double den = HD[k] > 1e-30 ? HD[k] : 1e-30;
+                D[(int64_t)k * Nk + l] = D[(int64_t)k * Nk + l] * B[(int64_t)k * Nk + l] / den;
+            }
+        }
+        if (obj) obj[2 * it + 1] = oracle_nmf_objective(Y, Np, Nk, ld_y, K, V, D, nthreads);
+    }
+    free(G);
+    free(H);
+    free(B);
+    return 0;
+}
+
+/*
+ * Sampled single-iteration checks at sizes the full oracle cannot reach
+ * (tests at BASELINE.json full size): from the GPU's (V_n, D_n) the oracle
+ * recomputes, for the listed rows, the V half-step of iteration n+1
+ * (row-local, PAPER.md:191 via reading R2), and for the listed bins, the
+ * D half-step given the full V_{n+1} (column-local).  Same formulas as
+ * oracle_nmf, restricted to the requested outputs.
+ */
+int oracle_nmf_vstep_rows(const float* Y, int64_t Np, int64_t Nk, int64_t ld_y, int K,
+                          const double* V, const double* D, const int64_t* rows, int64_t nrows,
+                          double* Vout /* nrows x K */, int nthreads) {
+    set_threads(nthreads);
+    double G[256];
+    for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b) {
+            double s = 0.0;
+            for (int64_t l = 0; l < Nk; ++l) s += D[(int64_t)a * Nk + l] * D[(int64_t)b * Nk + l];
+            G[a * K + b] = s;
+        }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < nrows; ++i) {
+        int64_t p = rows[i];
+        for (int k = 0; k < K; ++k) {
+            double A = 0.0, VG = 0.0;
+            for (int64_t l = 0; l < Nk; ++l) A += yplus(Y, ld_y, p, l) * D[(int64_t)k * Nk + l];
+            for (int j = 0; j < K; ++j) VG += V[p * K + j] * G[j * K + k];
+            double den = VG > 1e-30 ? VG : 1e-30;
+            Vout[i * K + k] = V[p * K + k] * A / den;
+        }
+    }
+    (void)Np;
+    return 0;
+}
+
+int oracle_nmf_dstep_cols(const float* Y, int64_t Np, int64_t Nk, int64_t ld_y, int K,
+                          const double* V /* V_{n+1}, Np x K */, const double* D /* D_n */,
+                          const int64_t* cols, int64_t ncols, double* Dout /* K x ncols */,
+                          int nthreads) {
+    set_threads(nthreads);
+    double H[256];
+    for (int a = 0; a < K; ++a)
+        for (int b = 0; b < K; ++b) {
+            double s = 0.0;
+            for (int64_t p = 0; p < Np; ++p) s += V[p * K + a] * V[p * K + b];
+            H[a * K + b] = s;
+        }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < ncols; ++i) {
+        int64_t l = cols[i];
+        for (int k = 0; k < K; ++k) {
+            double B = 0.0, HD = 0.0;
+            for (int64_t p = 0; p < Np; ++p) B += V[p * K + k] * yplus(Y, ld_y, p, l);
+            for (int j = 0; j < K; ++j) HD += H[k * K + j] * D[(int64_t)j * Nk + l];
+            double den = HD > 1e-30 ? HD : 1e-30;
+            Dout[(int64_t)k * ncols + i] = D[(int64_t)k * Nk + l] * B / den;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Tomographic reconstruction by FBP (reading R10-R16).    */
+/* ------------------------------------------------------------------------ */
+
+/* Kak-Slaney discrete Ram-Lak kernel with detector pitch tau = 1 (R11):
+ * h[0] = 1/4, h[even != 0] = 0, h[odd d] = -1/(pi^2 d^2). */
+double oracle_ramp_kernel(int64_t d) {
+    if (d == 0) return 0.25;
+    if (d % 2 == 0) return 0.0;
+    return -1.0 / (OR_PI * OR_PI * (double)d * (double)d);
+}
+
+/* Direct linear convolution q[c] = sum_{m=0}^{Nc-1} h[c-m] s[m] of each of
+ * nrows contiguous rows of length Nc (R11: no FFT in the oracle). */
+static void ramp_filter_row(const double* sr, double* qr, int64_t Nc) {
+    for (int64_t c = 0; c < Nc; ++c) {
+        double acc = 0.0;
+        for (int64_t m = 0; m < Nc; ++m) acc += oracle_ramp_kernel(c - m) * sr[m];
+        qr[c] = acc;
+    }
+}
+
+void oracle_ramp_filter_rows(const double* s, double* q, int64_t nrows, int64_t Nc, int nthreads) {
+    set_threads(nthreads);
+#pragma omp parallel for schedule(static)
+    for (int64_t row = 0; row < nrows; ++row) ramp_filter_row(s + row * Nc, q + row * Nc, Nc);
+}
+
+/* theta_v = v*pi/Nv (R13) unless the caller passes angles. */
+static double view_angle(const double* angles, int64_t v, int64_t Nv) {
+    return angles ? angles[v] : (double)v * OR_PI / (double)Nv;
+}
+
+/* Voxel-driven linear-interpolation backprojection of one slice (R12, R14,
+ * R16): X[i][j] = (pi/Nv) sum_v [(1-w) q_v[i0] + w q_v[i0+1]],
+ * u = x_j cos(theta_v) + y_i sin(theta_v) + (Nc-1)/2, i0 = floor(u),
+ * w = u - i0, q outside [0, Nc-1] = 0, x_j = j-(Nc-1)/2, y_i = i-(Nc-1)/2.
+ * q is [Nv][Nc] (filtered sinogram of the slice). */
+void oracle_backproject_slice(const double* q, int64_t Nv, int64_t Nc, const double* angles,
+                              double* X) {
+    double half = 0.5 * (double)(Nc - 1);
+    for (int64_t i = 0; i < Nc; ++i)
+        for (int64_t j = 0; j < Nc; ++j) {
+            double x = (double)j - half, y = (double)i - half, acc = 0.0;
+            for (int64_t v = 0; v < Nv; ++v) {
+                double th = view_angle(angles, v, Nv);
+                double u = x * cos(th) + y * sin(th) + half;
+                double fl = floor(u);
+                int64_t i0 = (int64_t)fl;
+                double w = u - fl;
+                double a = (i0 >= 0 && i0 < Nc) ? q[v * Nc + i0] : 0.0;
+                double b = (i0 + 1 >= 0 && i0 + 1 < Nc) ? q[v * Nc + i0 + 1] : 0.0;
+                acc += (1.0 - w) * a + w * b;
+            }
+            X[i * Nc + j] = OR_PI / (double)Nv * acc;
+        }
+}
+
+/* Exact matrix adjoint of oracle_backproject_slice (without the pi/Nv
+ * factor's transpose being special: it is a scalar): a voxel-driven
+ * "splat" forward projector.  Check-only tool for the adjoint pin. */
+void oracle_splat_project_slice(const double* X, int64_t Nv, int64_t Nc, const double* angles,
+                                double* P) {
+    double half = 0.5 * (double)(Nc - 1);
+    for (int64_t t = 0; t < Nv * Nc; ++t) P[t] = 0.0;
+    for (int64_t v = 0; v < Nv; ++v) {
+        double th = view_angle(angles, v, Nv);
+        for (int64_t i = 0; i < Nc; ++i)
+            for (int64_t j = 0; j < Nc; ++j) {
+                double x = (double)j - half, y = (double)i - half;
+                double u = x * cos(th) + y * sin(th) + half;
+                double fl = floor(u);
+                int64_t i0 = (int64_t)fl;
+                double w = u - fl, val = OR_PI / (double)Nv * X[i * Nc + j];
+                if (i0 >= 0 && i0 < Nc) P[v * Nc + i0] += (1.0 - w) * val;
+                if (i0 + 1 >= 0 && i0 + 1 < Nc) P[v * Nc + i0 + 1] += w * val;
+            }
+    }
+}
+
+/* Naive ray-sampled Radon transform of an Nc x Nc image (check-only tool):
+ * P[v][c] = sum_s f(t e_theta + s e_perp) * ds, bilinear sampling of the
+ * pixel grid (pixel (i,j) at (x_j, y_i)), ds = step, s in [-Nc, Nc]. */
+void oracle_radon_naive(const double* img, int64_t Nc, int64_t Nv, const double* angles,
+                        double step, double* P, int nthreads) {
+    set_threads(nthreads);
+    double half = 0.5 * (double)(Nc - 1);
+#pragma omp parallel for schedule(static)
+    for (int64_t vc = 0; vc < Nv * Nc; ++vc) {
+        int64_t v = vc / Nc, c = vc % Nc;
+        double th = view_angle(angles, v, Nv);
+        double ct = cos(th), st = sin(th), t = (double)c - half, acc = 0.0;
+        int64_t ns = (int64_t)ceil((double)Nc / step);
+        for (int64_t n = -ns; n <= ns; ++n) {
+            double s = (double)n * step;
+            double x = t * ct - s * st, y = t * st + s * ct;
+            double fj = x + half, fi = y + half;
+            double j0 = floor(fj), i0 = floor(fi);
+            double wj = fj - j0, wi = fi - i0;
+            int64_t J = (int64_t)j0, I = (int64_t)i0;
+            double val = 0.0;
+            for (int di = 0; di < 2; ++di)
+                for (int dj = 0; dj < 2; ++dj) {
+                    int64_t ii = I + di, jj = J + dj;
+                    if (ii < 0 || ii >= Nc || jj < 0 || jj >= Nc) continue;
+                    double wgt = (di ? wi : 1.0 - wi) * (dj ? wj : 1.0 - wj);
+                    val += wgt * img[ii * Nc + jj];
+                }
+            acc += val * step;
+        }
+        P[vc] = acc;
+    }
+}
+
+/* FBP of K subspace sinograms (Algorithm 1, "Tomographic Reconstruction",
+ * PAPER.md:240-243, with FBP per reading R10).  V is the N_p x K subspace
+ * view matrix V^s; column k reshaped to (N_v, N_r, N_c) is
+ * sinogram k.  X out: [K][N_r][N_c][N_c] (x^s in R^{N_x x N_s}, PAPER.md:223,
+ * stored channel-planar). */
+int oracle_fbp(const double* V, int64_t Nv, int64_t Nr, int64_t Nc, int K, const double* angles,
+               double* X, int nthreads) {
+    if (Nv < 1 || Nr < 1 || Nc < 1 || K < 1) return 1;
+    set_threads(nthreads);
+#pragma omp parallel for schedule(dynamic) collapse(2)
+    for (int k = 0; k < K; ++k)
+        for (int64_t r = 0; r < Nr; ++r) {
+            double* s = (double*)malloc(sizeof(double) * Nv * Nc);
+            double* q = (double*)malloc(sizeof(double) * Nv * Nc);
+            for (int64_t v = 0; v < Nv; ++v)
+                for (int64_t c = 0; c < Nc; ++c) s[v * Nc + c] = V[((v * Nr + r) * Nc + c) * K + k];
+            for (int64_t v = 0; v < Nv; ++v) ramp_filter_row(s + v * Nc, q + v * Nc, Nc);
+            oracle_backproject_slice(q, Nv, Nc, angles, X + ((int64_t)k * Nr + r) * Nc * Nc);
+            free(s);
+            free(q);
+        }
+    return 0;
+}
+
+/* Subspace expansion, Eq. 6: x^h = x^s (D^s)^T, as the
+ * triple loop xh[n][l] = sum_k X[k][n] D[k][l] over the window of slices
+ * [s0, s0+ns) and bins [b0, b0+nb).  Xh out: [ns*Nc*Nc][nb]. */
+int oracle_synthesize(const double* X, const double* D, int64_t Nr, int64_t Nc, int64_t Nk, int K,
+                      int64_t s0, int64_t ns, int64_t b0, int64_t nb, double* Xh, int nthreads) {
+    if (s0 < 0 || ns < 0 || s0 + ns > Nr || b0 < 0 || nb < 0 || b0 + nb > Nk) return 1;
+    set_threads(nthreads);
+    int64_t Nx = Nr * Nc * Nc, n0 = s0 * Nc * Nc, nn = ns * Nc * Nc;
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < nn; ++n)
+        for (int64_t l = 0; l < nb; ++l) {
+            double acc = 0.0;
+            for (int k = 0; k < K; ++k) acc += X[(int64_t)k * Nx + n0 + n] * D[(int64_t)k * Nk + b0 + l];
+            Xh[n * nb + l] = acc;
+        }
+    return 0;
+}
+
+/* Direct hyperspectral reconstruction, the paper's baseline (PAPER.md:441-442:
+ * "DHR performs N_k individual 3D reconstructions, one for each wavelength
+ * bin in p ... using FBP"): for each bin l in the window the sinogram
+ * Y[(v,r,c), l] (raw, unclamped: R6) is ramp-filtered and backprojected.
+ * Xh out: [ns*Nc*Nc][nb]. */
+int oracle_dhr(const float* Y, int64_t ld_y, int64_t Nv, int64_t Nr, int64_t Nc, int64_t Nk,
+               const double* angles, int64_t s0, int64_t ns, int64_t b0, int64_t nb, double* Xh,
+               int nthreads) {
+    if (s0 < 0 || ns < 0 || s0 + ns > Nr || b0 < 0 || nb < 0 || b0 + nb > Nk) return 1;
+    set_threads(nthreads);
+    int64_t NN = Nc * Nc;
+#pragma omp parallel for schedule(dynamic) collapse(2)
+    for (int64_t r = s0; r < s0 + ns; ++r)
+        for (int64_t l = b0; l < b0 + nb; ++l) {
+            double* s = (double*)malloc(sizeof(double) * Nv * Nc);
+            double* q = (double*)malloc(sizeof(double) * Nv * Nc);
+            double* x = (double*)malloc(sizeof(double) * NN);
+            for (int64_t v = 0; v < Nv; ++v)
+                for (int64_t c = 0; c < Nc; ++c) s[v * Nc + c] = (double)Y[((v * Nr + r) * Nc + c) * ld_y + l];
+            for (int64_t v = 0; v < Nv; ++v) ramp_filter_row(s + v * Nc, q + v * Nc, Nc);
+            oracle_backproject_slice(q, Nv, Nc, angles, x);
+            for (int64_t n = 0; n < NN; ++n) Xh[((r - s0) * NN + n) * nb + (l - b0)] = x[n];
+            free(s);
+            free(q);
+            free(x);
+        }
+    return 0;
+}
