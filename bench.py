@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""Benchmark of the FHR hot path (BASELINE.json metric: hyperspectral voxel*lambda
+reconstructed per second on 1xB200, plus % roofline).
+
+One step = the whole hot path on one batch of synthetic input already resident
+in HBM: subspace_decompose (n_iter Lee-Seung iterations from the seeded init)
+-> fbp of the K subspace sinograms -> synthesize x^h over all slices and bins.
+value = N_x * N_k * ranks / (max-over-ranks time per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl hsnct|reference]
+
+--impl reference times the fp64 CPU oracle (the tier's reference arm) on a bounded
+sample of the same workload.  Under torchrun every rank runs an independent
+replica of the workload (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "hyperspectral voxel*lambda reconstructed/sec (1xB200) + % roofline per stage"
+UNIT = "voxel*lambda/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[i-1]")
+    ap.add_argument("--impl", default="hsnct", choices=["hsnct", "reference"])
+    ap.add_argument("--n-iter", type=int, default=None, help="override NMF iterations (testing only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-dhr", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def max_over_ranks(x: float, world: int, device=None) -> float:
+    """Max of a scalar over all ranks (NCCL on GPU, gloo on CPU)."""
+    if world <= 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=d.get("hbm_gbs", 6650.0), sm_max_mhz=d.get("sm_max_mhz", 1965.0),
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload_desc(cfg, n_iter):
+    return (f"C{cfg.idx}: {cfg.Nc}x{cfg.Nc}x{cfg.Nr} volume, {cfg.Nv} views over 180 deg, "
+            f"Nk={cfg.Nk}, K={cfg.K}, {n_iter} NMF iterations, {cfg.M} materials, "
+            f"Poisson {cfg.counts:g} counts/bin")
+
+
+# ----------------------------------------------------------------- CPU oracle
+def oracle_sample(pr, n_iter, nthreads=0):
+    """Bounded oracle sample of one step: 2 NMF iterations on the full Y (time
+    extrapolated to n_iter), FBP of <= 2 slices and synthesis of <= 2 slices
+    (scaled to N_r).  Returns (seconds for one full step, description, threads)."""
+    import numpy as np
+
+    import oracle
+    cfg = pr["cfg"]
+    Y = pr["Y"].cpu().numpy()
+    V0 = pr["V0"].cpu().numpy()
+    D0 = pr["D0"].cpu().numpy()
+    it_s = 2
+    t0 = time.perf_counter()
+    V, D = oracle.nmf(Y, V0, D0, it_s, nthreads=nthreads)
+    t_nmf = (time.perf_counter() - t0) / it_s
+    ns = min(cfg.Nr, 2)
+    Vs = V.reshape(cfg.Nv, cfg.Nr, cfg.Nc, cfg.K)[:, :ns].reshape(-1, cfg.K)
+    t0 = time.perf_counter()
+    X = oracle.fbp(Vs, cfg.Nv, ns, cfg.Nc, nthreads=nthreads)
+    t_fbp = (time.perf_counter() - t0) * cfg.Nr / ns
+    t0 = time.perf_counter()
+    oracle.synthesize(X, D, 0, ns, nthreads=nthreads)
+    t_syn = (time.perf_counter() - t0) * cfg.Nr / ns
+    total = t_nmf * n_iter + t_fbp + t_syn
+    desc = (f"oracle (fp64 C, OpenMP) on the {cfg.name} inputs: {it_s} of {n_iter} NMF iterations on the "
+            f"full Y ({t_nmf:.3f} s/iter, x{n_iter} extrapolated), FBP + synthesis of {ns} of {cfg.Nr} "
+            f"slice(s) scaled x{cfg.Nr / ns:g}")
+    return total, desc, (nthreads or oracle.max_threads())
+
+
+def run_reference(args, cfg, n_iter, rank, world):
+    import synthdata as sd
+    if rank != 0:
+        return 0
+    pr = sd.make_problem(cfg)
+    for _ in range(args.warmup):
+        pass  # the oracle has no warm-up state; warm-up steps are skipped deliberately
+    times = []
+    desc, cores = "", 0
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        t, desc, cores = oracle_sample(pr, n_iter)
+        times.append(t)
+    wall = time.perf_counter() - t_start
+    T = statistics.mean(times)
+    value = cfg.Nx * cfg.Nk / T
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": T * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Bragg-edge phantom, Poisson counts)",
+            "config": {"workload": workload_desc(cfg, n_iter), "config_index": cfg.idx},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": desc, "wall_s": wall},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synthdata as sd
+    from paper_2410_22500_b200 import Hsnct
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+
+    pr = sd.make_problem(cfg, device=dev)
+    Y, V0, D0 = pr["Y"], pr["V0"], pr["D0"]
+    h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=local_rank)
+    V = torch.empty_like(V0)
+    D = torch.empty_like(D0)
+    X = torch.empty((cfg.K, cfg.Nr, cfg.Nc, cfg.Nc), dtype=torch.float32, device=dev)
+    # x^h: one window buffer reused across windows when the volume exceeds the budget
+    win = max(1, min(cfg.Nr, (8 << 30) // (cfg.Nc * cfg.Nc * cfg.Nk * 4)))
+    Xh = torch.empty((win * cfg.Nc * cfg.Nc, cfg.Nk), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(rec=None):
+        V.copy_(V0)
+        D.copy_(D0)
+        if rec is not None:
+            rec[0].record(stream)
+        h.subspace_decompose(Y, V, D, n_iter)
+        if rec is not None:
+            rec[1].record(stream)
+        h.fbp(V, X)
+        if rec is not None:
+            rec[2].record(stream)
+        for s0 in range(0, cfg.Nr, win):
+            ns = min(win, cfg.Nr - s0)
+            h.synthesize(X, D, s0, ns, 0, cfg.Nk, Xh=Xh[:ns * cfg.Nc * cfg.Nc])
+        if rec is not None:
+            rec[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    h.sync()
+    torch.cuda.synchronize()
+    recs = [[ev() for _ in range(4)] for _ in range(args.steps)]
+    l0 = h.kernel_launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for i in range(args.steps):
+            step(recs[i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = h.kernel_launches - l0
+    h.sync()
+    ms_total = e0.elapsed_time(e1)
+    ms_step = max_over_ranks(ms_total / args.steps, world, dev)
+    t_nmf = statistics.mean(r[0].elapsed_time(r[1]) for r in recs) * 1e-3
+    t_fbp = statistics.mean(r[1].elapsed_time(r[2]) for r in recs) * 1e-3
+    t_syn = statistics.mean(r[2].elapsed_time(r[3]) for r in recs) * 1e-3
+    value = cfg.Nx * cfg.Nk * world / (ms_step * 1e-3)
+
+    # rooflines (algorithmic bytes)
+    Np, Nk, K, Nx = cfg.Np, cfg.Nk, cfg.K, cfg.Nx
+    nmf_bytes_iter = 4.0 * Np * Nk + 8.0 * Np * K
+    nmf_gbs = nmf_bytes_iter * n_iter / t_nmf / 1e9
+    syn_bytes = 4.0 * Nx * Nk + 4.0 * K * Nx
+    syn_gbs = syn_bytes / t_syn / 1e9
+    fbp_bytes = 4.0 * K * Np + 4.0 * K * Nx
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"C{cfg.idx}", {}).get("nmf_iter_dram_bytes")
+    roof = {"bound": "hbm", "kernel": "NMF iteration (k_vstep + k_bpart + k_dupdate)",
+            "achieved": nmf_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": nmf_gbs / peaks["hbm_gbs"], "traffic": traffic,
+            "algorithmic_bytes_per_unit": nmf_bytes_iter, "unit_of_work": "one NMF iteration",
+            "peak_source": peaks["source"]}
+    stages = {"nmf_s": t_nmf, "nmf_per_iter_us": t_nmf / n_iter * 1e6, "fbp_s": t_fbp,
+              "synth_s": t_syn, "nmf_hbm_frac": nmf_gbs / peaks["hbm_gbs"],
+              "synth_hbm_frac": syn_gbs / peaks["hbm_gbs"],
+              "fbp_hbm_frac": fbp_bytes / t_fbp / 1e9 / peaks["hbm_gbs"]}
+
+    # GPU DHR baseline (same data, outside the timed region)
+    dhr = None
+    if not args.no_dhr and rank == 0:
+        nb = min(cfg.Nk, 64) if cfg.Nr > 8 else cfg.Nk
+        ns = min(cfg.Nr, 8)
+        out = torch.empty((ns * cfg.Nc * cfg.Nc, nb), dtype=torch.float32, device=dev)
+        h.dhr(Y, 0, ns, 0, nb, Xh=out)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        h.dhr(Y, 0, ns, 0, nb, Xh=out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t = a.elapsed_time(b) * 1e-3
+        dhr = {"value": ns * cfg.Nc * cfg.Nc * nb / t, "unit": UNIT,
+               "sample": f"{ns} slice(s) x {nb} bins, rate extrapolates linearly"}
+
+    # end to end through the public API on pinned HOST buffers (hsnct_fhr_host)
+    e2e = None
+    if not args.no_e2e:
+        Yh = Y.cpu().pin_memory()
+        V0h, D0h = V0.cpu().pin_memory(), D0.cpu().pin_memory()
+        Xh_host = torch.empty((cfg.Nx, cfg.Nk), dtype=torch.float32, pin_memory=True) \
+            if cfg.Nx * cfg.Nk * 4 <= (48 << 30) else None
+        if Xh_host is not None:
+            del Xh
+            torch.cuda.empty_cache()
+            h.fhr_host(Yh, V0h, D0h, n_iter, Xh=Xh_host)
+            n_e2e = max(1, min(args.steps, 3))
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                h.fhr_host(Yh, V0h, D0h, n_iter, Xh=Xh_host)
+            t_e2e = max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
+            e2e = {"value": cfg.Nx * cfg.Nk * world / t_e2e, "unit": UNIT,
+                   "h2d_bytes_per_step": 4 * (Np * Nk + Np * K + K * Nk),
+                   "d2h_bytes_per_step": 4 * Nx * Nk, "ms_per_step": t_e2e * 1e3}
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        T, desc, cores = oracle_sample(pr, n_iter)
+        cpu = {"value": cfg.Nx * cfg.Nk / T, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic (seeded Bragg-edge ellipse phantom, Poisson counts, -log)",
+                "config": {"workload": workload_desc(cfg, n_iter), "config_index": cfg.idx,
+                           "Nc": cfg.Nc, "Nr": cfg.Nr, "Nv": cfg.Nv, "Nk": cfg.Nk, "K": cfg.K,
+                           "n_iter": n_iter, "parallelism": f"replicas x{world}",
+                           "l2": f"inputs larger than L2 (Y = {4 * Np * Nk / 1e6:.0f} MB > 126 MB)"},
+                "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "gpu_dhr": dhr, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    import synthdata as sd
+    cfg = sd.CONFIGS[args.config]
+    n_iter = args.n_iter if args.n_iter is not None else cfg.n_iter
+    rank, world, local_rank = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, cfg, n_iter, rank, world)
+    return run_hsnct(args, cfg, n_iter, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

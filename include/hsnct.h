@@ -1,0 +1,178 @@
+/*
+ * hsnct.h -- C ABI of libhsnct.so, the B200 (sm_100a) hot path of fast
+ * hyperspectral neutron tomography (FHR), arXiv 2410.22500.
+ *
+ * The calls follow the paper's statement of the problem:
+ *   Algorithm 1, "Input p, N_s -> Output x^h":
+ *     hsnct_subspace_decompose   subspace extraction, Eq. 4
+ *     hsnct_fbp                  tomographic reconstruction of the N_s subspace
+ *                                sinograms (FBP per DESIGN.md R10)
+ *     hsnct_synthesize           subspace expansion, Eq. 6
+ *   and the paper's baseline:
+ *     hsnct_dhr                  direct hyperspectral reconstruction, one FBP per
+ *                                wavelength bin
+ *   plus hsnct_fhr_host, the whole of Algorithm 1 on HOST buffers (the
+ *   end-to-end entry point: host->device copy, the three stages, device->host).
+ *
+ * Notation: N_v views, N_r detector rows (= slices),
+ * N_c detector columns (= image width), N_k wavelength bins,
+ * N_p = N_v N_r N_c projections, N_x = N_r N_c N_c voxels, K = N_s subspace
+ * dimension.
+ *
+ * Layouts (all fp32, row-major, caller-owned DEVICE memory unless stated):
+ *   Y   [N_p][ld_y]   projection data p, row p = (v*N_r + r)*N_c + c,
+ *                     bin index fastest.  ld_y >= N_k, ld_y % 4 == 0,
+ *                     16-byte aligned; all N_p*ld_y floats must be readable (the
+ *                     padding columns are read and ignored).
+ *   V   [N_p][K]      subspace views V^s, row p as for Y.
+ *   D   [K][N_k]      subspace basis, stored as (D^s)^T.
+ *   X   [K][N_r][N_c][N_c]  subspace reconstructions x^s,
+ *                     channel-planar; voxel (r, i, j) at x = j-(N_c-1)/2,
+ *                     y = i-(N_c-1)/2 (R14).
+ *   Xh  [n_slices*N_c*N_c][ld_xh]  a window of x^h: voxels of
+ *                     slices [slice0, slice0+n_slices), bins [bin0, bin0+n_bins),
+ *                     bin fastest; ld_xh >= n_bins.
+ * Geometry (R11-R16): theta_v = v*pi/N_v unless angles are given;
+ * Kak-Slaney Ram-Lak filter (tau = 1); linear interpolation; scale pi/N_v;
+ * detector samples outside [0, N_c-1] are zero; no FOV mask.
+ *
+ * Ownership: every array is allocated and freed by the caller (PyTorch).
+ * The library allocates only small per-handle constant tables (angles,
+ * filter spectrum, FFT twiddles, a status word) in hsnct_create and frees
+ * them in hsnct_destroy.  Scratch space is the caller's workspace buffer
+ * (device, 256-byte aligned, size from hsnct_workspace_bytes).
+ *
+ * Streams: every call only ENQUEUES work on the caller's CUDA stream
+ * (a cudaStream_t passed as void*; NULL = legacy default stream) and
+ * returns; a handle must be used by one stream at a time.
+ *
+ * Errors: argument errors (null / misaligned pointers, shapes, windows,
+ * workspace too small, overlapping outputs) are detected on the host before
+ * any launch and returned synchronously as HSNCT_E_ARG (SPEC "config" class).
+ * Data-dependent errors are recorded in a device status word and returned
+ * by hsnct_sync: HSNCT_E_DATA for non-finite Y / V0 / D0 or an all-zero Y+
+ * (SPEC "data" class), HSNCT_E_NUMERIC for a non-finite V or D produced by
+ * the iteration (SPEC "numerical" class).  HSNCT_E_CUDA reports a CUDA
+ * runtime failure (launch or copy), details in hsnct_last_error.
+ */
+#ifndef HSNCT_H_
+#define HSNCT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSNCT_ABI_VERSION 1
+#define HSNCT_MAX_SUB 16 /* K = N_s <= 16 */
+
+typedef struct hsnct_s* hsnct_t;
+
+typedef enum {
+    HSNCT_OK = 0,
+    HSNCT_E_ARG = 1,     /* bad shape / range / null / misaligned / aliasing / window / workspace */
+    HSNCT_E_DATA = 2,    /* non-finite input, negative init, Y+ identically zero (deferred)      */
+    HSNCT_E_NUMERIC = 3, /* NaN/Inf produced during the iteration (deferred)                     */
+    HSNCT_E_CUDA = 4,    /* CUDA runtime error                                                   */
+    HSNCT_E_NOMEM = 5    /* host or handle-table allocation failed                               */
+} hsnct_status;
+
+typedef enum {
+    HSNCT_OP_DECOMPOSE = 0, /* hsnct_subspace_decompose                    */
+    HSNCT_OP_FBP = 1,       /* hsnct_fbp                                   */
+    HSNCT_OP_DHR = 2,       /* hsnct_dhr, any window (the minimum is used) */
+    HSNCT_OP_FHR_HOST = 3   /* hsnct_fhr_host                              */
+} hsnct_op;
+
+typedef struct {
+    int32_t n_views; /* N_v >= 2                 */
+    int32_t n_rows;  /* N_r >= 1                 */
+    int32_t n_cols;  /* 2 <= N_c <= 2048         */
+    int32_t n_bins;  /* N_k >= 1                 */
+    int32_t n_sub;   /* 1 <= K <= min(16, N_k)   */
+    const double* angles; /* HOST array of N_v view angles in radians, copied at create;
+                             NULL => theta_v = v*pi/N_v (R13)            */
+} hsnct_geom;
+
+/* Validates the geometry, selects device `device` and builds the constant
+ * tables (cos/sin per view; the DFT of the zero-padded Kak-Slaney kernel,
+ * P = next_pow2(2 N_c); FFT twiddles) in fp64 on the host.  *out receives the
+ * handle.  E_ARG on a bad geometry, E_CUDA / E_NOMEM on allocation failure. */
+hsnct_status hsnct_create(const hsnct_geom* g, int device, hsnct_t* out);
+
+/* Frees the handle's tables.  Safe on NULL.  Synchronizes the device. */
+void hsnct_destroy(hsnct_t h);
+
+/* Workspace bytes the caller must provide for `op` (hsnct_op).  0 on a bad
+ * handle / op.  HSNCT_OP_DHR returns the size for a one-slice window; larger
+ * workspaces let hsnct_dhr process more slices per pass. */
+size_t hsnct_workspace_bytes(hsnct_t h, int op);
+
+/* Subspace extraction, Eq. 4: n_iter Lee-Seung
+ * multiplicative-update iterations (R1-R3, V half first) on
+ * Y+ = max(Y, 0) (R6), starting from the caller's V (= V0, strictly > 0) and
+ * D (= D0, strictly > 0), both overwritten in place with V_n, D_n (raw,
+ * unnormalised iterates, R9).  One iteration:
+ *   V <- V .* (Y+ D^T) ./ max(V (D D^T), 1e-30);  D <- D .* (V^T Y+) ./ max((V^T V) D, 1e-30).
+ * obj_trace (device fp64, 2*n_iter entries, nullable) receives ||Y+ - V D||_F^2
+ * after each half-step, evaluated in fp64 from the Gram identity.
+ * n_iter == 0 is a no-op.  Deterministic: static schedule, fixed reduction
+ * order, no floating-point atomics.  Resume = call again with the same V, D. */
+hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, float* V, float* D,
+                                      int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
+                                      void* stream);
+
+/* FBP of the K subspace sinograms (Algorithm 1 lines "Tomographic
+ * Reconstruction", FBP per R10): column k of V, reshaped
+ * (N_v, N_r, N_c), is ramp-filtered along c and backprojected into X[k].
+ * X must not overlap V or ws. */
+hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_bytes, void* stream);
+
+/* Subspace expansion, Eq. 6, x^h = x^s (D^s)^T, on a
+ * window: Xh[n][b] = sum_k X[k][slice0*N_c*N_c + n] * D[k][bin0 + b].
+ * Empty windows (n_slices == 0 or n_bins == 0) are a no-op. */
+hsnct_status hsnct_synthesize(hsnct_t h, const float* X, const float* D, int slice0, int n_slices,
+                              int bin0, int n_bins, float* Xh, int64_t ld_xh, void* stream);
+
+/* Direct hyperspectral reconstruction, the baseline: every
+ * bin b of the window is reconstructed separately by FBP of the raw
+ * (unclamped, R6) sinogram Y[., bin0 + b]; output layout as hsnct_synthesize. */
+hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int n_slices, int bin0,
+                       int n_bins, float* Xh, int64_t ld_xh, void* ws, size_t ws_bytes, void* stream);
+
+/* The whole of Algorithm 1 on HOST buffers (end to end): copies Y_host
+ * [N_p][ld_y], V0_host [N_p][K], D0_host [K][N_k] to the device workspace,
+ * runs decompose(n_iter) -> fbp -> synthesize over all slices and bins in
+ * windows, and copies x^h back to Xh_host [N_x][N_k] (ld = N_k), V and D back
+ * to V_host / D_host (nullable).  Host buffers should be page-locked for
+ * full copy bandwidth.  Blocks until the result is on the host; returns the
+ * deferred data/numeric status like hsnct_sync. */
+hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
+                            const float* D0_host, int n_iter, float* Xh_host, float* V_host,
+                            float* D_host, void* ws, size_t ws_bytes, void* stream);
+
+/* Waits for the stream, then returns and clears the deferred status
+ * (HSNCT_OK, HSNCT_E_DATA or HSNCT_E_NUMERIC), or HSNCT_E_CUDA. */
+hsnct_status hsnct_sync(hsnct_t h, void* stream);
+
+/* Number of kernels this handle has launched since create (for launch-count
+ * accounting in bench.py). */
+uint64_t hsnct_kernel_launches(hsnct_t h);
+
+/* Static description of a status code; never NULL. */
+const char* hsnct_status_string(hsnct_status st);
+
+/* Thread-local description of the last error raised by any call on this
+ * thread (argument that failed, CUDA error string); "" if none. */
+const char* hsnct_last_error(void);
+
+/* HSNCT_ABI_VERSION of the loaded library. */
+int hsnct_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HSNCT_H_ */

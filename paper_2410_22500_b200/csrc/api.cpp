@@ -1,0 +1,491 @@
+// C ABI of libhsnct.so (include/hsnct.h): argument validation, workspace
+// carving, constant tables and launch sequencing.  Every numerical step runs
+// in the CUDA kernels of nmf.cu / fbp.cu / synth.cu; this file does no
+// arithmetic on the data.
+#include "hsnct.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace hsnct;
+
+struct hsnct_s {
+    int device = 0;
+    Geometry g{};
+    DeviceTables t{};
+    NmfPlan nmf{};
+    unsigned* status_host = nullptr;  // pinned mirror of t.status
+    uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+hsnct_status fail(hsnct_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+hsnct_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(HSNCT_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CK(expr, where)                                   \
+    do {                                                  \
+        cudaError_t e_ = (expr);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+struct Range {
+    uintptr_t lo, hi;
+};
+Range rng(const void* p, size_t bytes) {
+    uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    return Range{a, a + bytes};
+}
+bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi && a.hi > a.lo && b.hi > b.lo; }
+
+int64_t Np_of(const Geometry& g) { return (int64_t)g.Nv * g.Nr * g.Nc; }
+int64_t Nx_of(const Geometry& g) { return (int64_t)g.Nr * g.Nc * g.Nc; }
+int kc_of(int K) { return (K + 3) & ~3; }
+int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
+
+size_t fbp_ws(const Geometry& g) { return a256((size_t)Np_of(g) * kc_of(g.K) * sizeof(float)); }
+size_t dhr_ws_per_slice(const Geometry& g) {
+    return (size_t)g.Nv * g.Nc * dhr_kc(g) * sizeof(float);
+}
+int64_t fhr_window_slices(const Geometry& g) {
+    const size_t per = (size_t)g.Nc * g.Nc * g.Nk * sizeof(float);
+    const size_t budget = size_t(2) << 30;
+    return std::max<int64_t>(1, std::min<int64_t>(g.Nr, (int64_t)(budget / std::max<size_t>(per, 1))));
+}
+struct FhrHostLayout {
+    size_t y, v, d, x, xh, nmf, fbp, total;
+    int Nkp;
+};
+FhrHostLayout fhr_layout(const Geometry& g, const NmfPlan& p) {
+    FhrHostLayout L{};
+    L.Nkp = (g.Nk + 3) & ~3;
+    L.y = a256((size_t)Np_of(g) * L.Nkp * sizeof(float));
+    L.v = a256((size_t)Np_of(g) * g.K * sizeof(float));
+    L.d = a256((size_t)g.K * g.Nk * sizeof(float));
+    L.x = a256((size_t)g.K * Nx_of(g) * sizeof(float));
+    L.xh = a256((size_t)fhr_window_slices(g) * g.Nc * g.Nc * g.Nk * sizeof(float));
+    L.nmf = a256(nmf_ws_bytes(g, p));
+    L.fbp = fbp_ws(g);
+    L.total = L.y + L.v + L.d + L.x + L.xh + L.nmf + L.fbp;
+    return L;
+}
+
+hsnct_status check_ws(void* ws, size_t have, size_t need, const char* op) {
+    if (need == 0) return HSNCT_OK;
+    if (!ws) return fail(HSNCT_E_ARG, "%s: workspace is NULL (need %zu bytes)", op, need);
+    if (!aligned(ws, 256)) return fail(HSNCT_E_ARG, "%s: workspace must be 256-byte aligned", op);
+    if (have < need) return fail(HSNCT_E_ARG, "%s: workspace %zu bytes < required %zu", op, have, need);
+    return HSNCT_OK;
+}
+
+hsnct_status check_window(const Geometry& g, int s0, int ns, int b0, int nb, int64_t ld, const char* op) {
+    if (s0 < 0 || ns < 0 || (int64_t)s0 + ns > g.Nr)
+        return fail(HSNCT_E_ARG, "%s: slice window [%d, %d+%d) outside [0, %d)", op, s0, s0, ns, g.Nr);
+    if (b0 < 0 || nb < 0 || (int64_t)b0 + nb > g.Nk)
+        return fail(HSNCT_E_ARG, "%s: bin window [%d, %d+%d) outside [0, %d)", op, b0, b0, nb, g.Nk);
+    if (ld < nb) return fail(HSNCT_E_ARG, "%s: ld_xh=%lld < n_bins=%d", op, (long long)ld, nb);
+    return HSNCT_OK;
+}
+
+hsnct_status check_y(const Geometry& g, const float* Y, int64_t ld, const char* op) {
+    if (!Y) return fail(HSNCT_E_ARG, "%s: Y is NULL", op);
+    if (!aligned(Y, 16)) return fail(HSNCT_E_ARG, "%s: Y must be 16-byte aligned", op);
+    if (ld < g.Nk || ld % 4 != 0)
+        return fail(HSNCT_E_ARG, "%s: ld_y=%lld must be >= N_k=%d and a multiple of 4", op, (long long)ld, g.Nk);
+    return HSNCT_OK;
+}
+
+// Enqueue decompose on device buffers (shared by the ABI call and fhr_host).
+hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, float* D, int n_iter,
+                           double* obj, void* ws, cudaStream_t s) {
+    if (n_iter == 0) return HSNCT_OK;
+    const NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
+    CK(nmf_launch_init(h->g, h->nmf, w, D, h->t.status, s), "decompose init");
+    h->launches += 1;
+    for (int it = 0; it < n_iter; ++it) {
+        CK(nmf_launch_iter(h->g, h->nmf, w, Y, ld, V, D, it == 0, obj ? obj + 2 * it : nullptr,
+                           h->t.status, h->t.counter, s),
+           "decompose iteration");
+        h->launches += NMF_LAUNCHES_PER_ITER;
+    }
+    return HSNCT_OK;
+}
+
+hsnct_status run_fbp(hsnct_t h, const float* V, float* X, void* ws, cudaStream_t s) {
+    const Geometry& g = h->g;
+    float* Q = static_cast<float*>(ws);
+    const int kc = kc_of(g.K);
+    CK(ramp_filter(g, h->t, V, g.K, g.K, 0, g.Nr, Q, kc, s), "fbp ramp filter");
+    CK(backproject(g, h->t, Q, kc, g.K, 0, g.Nr, 0, X, 0, 0, s), "fbp backprojection");
+    h->launches += 2;
+    return HSNCT_OK;
+}
+
+hsnct_status read_status(hsnct_t h, cudaStream_t s) {
+    CK(cudaMemcpyAsync(h->status_host, h->t.status, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "sync");
+    CK(cudaStreamSynchronize(s), "sync");
+    const unsigned st = *h->status_host;
+    if (st) {
+        CK(cudaMemsetAsync(h->t.status, 0, sizeof(unsigned), s), "sync");
+        CK(cudaStreamSynchronize(s), "sync");
+    }
+    if (st & (ST_Y_NONFINITE | ST_Y_ALLZERO | ST_INIT_BAD))
+        return fail(HSNCT_E_DATA, "data error (status 0x%x):%s%s%s", st,
+                    (st & ST_Y_NONFINITE) ? " non-finite Y;" : "",
+                    (st & ST_Y_ALLZERO) ? " Y+ is identically zero;" : "",
+                    (st & ST_INIT_BAD) ? " V0/D0 non-finite or negative;" : "");
+    if (st & ST_NUMERIC) return fail(HSNCT_E_NUMERIC, "numerical error: NaN/Inf produced in V or D");
+    return HSNCT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hsnct_abi_version(void) { return HSNCT_ABI_VERSION; }
+
+const char* hsnct_last_error(void) { return g_last_error.c_str(); }
+
+const char* hsnct_status_string(hsnct_status st) {
+    switch (st) {
+        case HSNCT_OK: return "ok";
+        case HSNCT_E_ARG: return "invalid argument";
+        case HSNCT_E_DATA: return "data error";
+        case HSNCT_E_NUMERIC: return "numerical error";
+        case HSNCT_E_CUDA: return "CUDA error";
+        case HSNCT_E_NOMEM: return "out of memory";
+    }
+    return "unknown status";
+}
+
+hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
+    g_last_error.clear();
+    if (!out) return fail(HSNCT_E_ARG, "create: out is NULL");
+    *out = nullptr;
+    if (!gp) return fail(HSNCT_E_ARG, "create: geometry is NULL");
+    const hsnct_geom& G = *gp;
+    if (G.n_views < 2) return fail(HSNCT_E_ARG, "create: n_views=%d < 2", G.n_views);
+    if (G.n_rows < 1) return fail(HSNCT_E_ARG, "create: n_rows=%d < 1", G.n_rows);
+    if (G.n_cols < 2 || G.n_cols > 1024) return fail(HSNCT_E_ARG, "create: n_cols=%d outside [2, 1024]", G.n_cols);
+    if (G.n_bins < 1) return fail(HSNCT_E_ARG, "create: n_bins=%d < 1", G.n_bins);
+    if (G.n_sub < 1 || G.n_sub > HSNCT_MAX_SUB || G.n_sub > G.n_bins)
+        return fail(HSNCT_E_ARG, "create: n_sub=%d outside [1, min(16, n_bins)]", G.n_sub);
+    if ((int64_t)G.n_sub * ((G.n_bins + 3) & ~3) > 51200)
+        return fail(HSNCT_E_ARG, "create: n_sub * n_bins = %lld exceeds 51200 (row-pass D tile)",
+                    (long long)G.n_sub * G.n_bins);
+    const int64_t Np = (int64_t)G.n_views * G.n_rows * G.n_cols;
+    if (Np > (int64_t)1 << 40) return fail(HSNCT_E_ARG, "create: N_p too large");
+    if (G.angles)
+        for (int v = 0; v < G.n_views; ++v)
+            if (!std::isfinite(G.angles[v])) return fail(HSNCT_E_ARG, "create: angle %d is not finite", v);
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(HSNCT_E_CUDA, "create: no CUDA device");
+    if (device < 0 || device >= ndev) return fail(HSNCT_E_ARG, "create: device %d outside [0, %d)", device, ndev);
+    DeviceGuard guard(device);
+
+    hsnct_t h = new (std::nothrow) hsnct_s();
+    if (!h) return fail(HSNCT_E_NOMEM, "create: host allocation failed");
+    h->device = device;
+    Geometry& g = h->g;
+    g.Nv = G.n_views;
+    g.Nr = G.n_rows;
+    g.Nc = G.n_cols;
+    g.Nk = G.n_bins;
+    g.K = G.n_sub;
+    g.P = 1;
+    g.logP = 0;
+    while (g.P < 2 * g.Nc) {
+        g.P <<= 1;
+        ++g.logP;
+    }
+    cudaDeviceGetAttribute(&g.num_sms, cudaDevAttrMultiProcessorCount, device);
+    h->nmf = nmf_plan(g, g.num_sms);
+
+    // Constant tables, built in fp64 on the host.
+    std::vector<float> cs(g.Nv), sn(g.Nv);
+    for (int v = 0; v < g.Nv; ++v) {
+        const double th = G.angles ? G.angles[v] : (double)v * M_PI / (double)g.Nv;
+        cs[v] = (float)std::cos(th);
+        sn[v] = (float)std::sin(th);
+    }
+    // Circularly arranged Kak-Slaney kernel (tau = 1): hc[n] = h[n], hc[P-n] = h[n], |n| <= Nc-1.
+    std::vector<double> hc(g.P, 0.0);
+    auto hk = [](long d) -> double {
+        if (d == 0) return 0.25;
+        if (d % 2 == 0) return 0.0;
+        return -1.0 / (M_PI * M_PI * (double)d * (double)d);
+    };
+    for (int n = 0; n < g.Nc; ++n) {
+        hc[n] = hk(n);
+        if (n > 0) hc[g.P - n] = hk(n);
+    }
+    std::vector<float> Hhat(g.P);
+    for (int f = 0; f < g.P; ++f) {
+        double s = 0.0;
+        for (int n = 0; n < g.P; ++n) {
+            if (hc[n] == 0.0) continue;
+            const long fn = ((long)f * n) % g.P;
+            s += hc[n] * std::cos(2.0 * M_PI * (double)fn / (double)g.P);
+        }
+        Hhat[f] = (float)(s / (double)g.P);  // inverse-FFT 1/P folded in
+    }
+    std::vector<float2> tw(g.P / 2);
+    for (int t = 0; t < g.P / 2; ++t) {
+        const double a = -2.0 * M_PI * (double)t / (double)g.P;
+        tw[t] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+    cudaError_t e = cudaSuccess;
+    auto al = [&](void** p, size_t b) {
+        if (e == cudaSuccess) e = cudaMalloc(p, b);
+    };
+    al((void**)&h->t.cos_t, g.Nv * sizeof(float));
+    al((void**)&h->t.sin_t, g.Nv * sizeof(float));
+    al((void**)&h->t.Hhat, g.P * sizeof(float));
+    al((void**)&h->t.twiddle, (g.P / 2) * sizeof(float2));
+    al((void**)&h->t.status, sizeof(unsigned));
+    al((void**)&h->t.counter, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->status_host, sizeof(unsigned), cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaMemcpy(h->t.cos_t, cs.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->t.sin_t, sn.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->t.Hhat, Hhat.data(), g.P * sizeof(float), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(h->t.twiddle, tw.data(), (g.P / 2) * sizeof(float2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(h->t.status, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        hsnct_destroy(h);
+        return cuda_fail(e, "create");
+    }
+    *out = h;
+    return HSNCT_OK;
+}
+
+void hsnct_destroy(hsnct_t h) {
+    if (!h) return;
+    DeviceGuard guard(h->device);
+    cudaDeviceSynchronize();
+    cudaFree(h->t.cos_t);
+    cudaFree(h->t.sin_t);
+    cudaFree(h->t.Hhat);
+    cudaFree(h->t.twiddle);
+    cudaFree(h->t.status);
+    cudaFree(h->t.counter);
+    if (h->status_host) cudaFreeHost(h->status_host);
+    delete h;
+}
+
+size_t hsnct_workspace_bytes(hsnct_t h, int op) {
+    if (!h) return 0;
+    switch (op) {
+        case HSNCT_OP_DECOMPOSE: return a256(nmf_ws_bytes(h->g, h->nmf));
+        case HSNCT_OP_FBP: return fbp_ws(h->g);
+        case HSNCT_OP_DHR: return a256(dhr_ws_per_slice(h->g));
+        case HSNCT_OP_FHR_HOST: return fhr_layout(h->g, h->nmf).total;
+        default: return 0;
+    }
+}
+
+hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, float* V, float* D,
+                                      int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
+                                      void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "decompose: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_y(g, Y, ld_y, "decompose");
+    if (st) return st;
+    if (!V || !D) return fail(HSNCT_E_ARG, "decompose: V or D is NULL");
+    if (!aligned(V, 4) || !aligned(D, 4)) return fail(HSNCT_E_ARG, "decompose: V, D must be 4-byte aligned");
+    if (n_iter < 0) return fail(HSNCT_E_ARG, "decompose: n_iter=%d < 0", n_iter);
+    if (obj_trace && !aligned(obj_trace, 8)) return fail(HSNCT_E_ARG, "decompose: obj_trace misaligned");
+    const size_t need = a256(nmf_ws_bytes(g, h->nmf));
+    if ((st = check_ws(ws, ws_bytes, need, "decompose"))) return st;
+    const Range rY = rng(Y, (size_t)Np_of(g) * ld_y * sizeof(float));
+    const Range rV = rng(V, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rD = rng(D, (size_t)g.K * g.Nk * sizeof(float));
+    const Range rW = rng(ws, need);
+    const Range rO = rng(obj_trace, obj_trace ? (size_t)2 * n_iter * sizeof(double) : 0);
+    if (overlap(rV, rD) || overlap(rV, rY) || overlap(rD, rY) || overlap(rW, rV) || overlap(rW, rD) ||
+        overlap(rW, rY) || overlap(rO, rV) || overlap(rO, rD) || overlap(rO, rW) || overlap(rO, rY))
+        return fail(HSNCT_E_ARG, "decompose: Y, V, D, obj_trace and workspace must not overlap");
+    DeviceGuard guard(h->device);
+    return run_decompose(h, Y, ld_y, V, D, n_iter, obj_trace, ws, (cudaStream_t)stream);
+}
+
+hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fbp: handle is NULL");
+    const Geometry& g = h->g;
+    if (!V || !X) return fail(HSNCT_E_ARG, "fbp: V or X is NULL");
+    if (!aligned(V, 4) || !aligned(X, 4)) return fail(HSNCT_E_ARG, "fbp: V, X must be 4-byte aligned");
+    hsnct_status st;
+    const size_t need = fbp_ws(g);
+    if ((st = check_ws(ws, ws_bytes, need, "fbp"))) return st;
+    const Range rV = rng(V, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rX = rng(X, (size_t)Nx_of(g) * g.K * sizeof(float));
+    const Range rW = rng(ws, need);
+    if (overlap(rV, rX) || overlap(rW, rX) || overlap(rW, rV))
+        return fail(HSNCT_E_ARG, "fbp: V, X and workspace must not overlap");
+    DeviceGuard guard(h->device);
+    return run_fbp(h, V, X, ws, (cudaStream_t)stream);
+}
+
+hsnct_status hsnct_synthesize(hsnct_t h, const float* X, const float* D, int slice0, int n_slices,
+                              int bin0, int n_bins, float* Xh, int64_t ld_xh, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "synthesize: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_window(g, slice0, n_slices, bin0, n_bins, ld_xh, "synthesize");
+    if (st) return st;
+    if (n_slices == 0 || n_bins == 0) return HSNCT_OK;
+    if (!X || !D || !Xh) return fail(HSNCT_E_ARG, "synthesize: X, D or Xh is NULL");
+    if (!aligned(X, 4) || !aligned(D, 4) || !aligned(Xh, 4))
+        return fail(HSNCT_E_ARG, "synthesize: X, D, Xh must be 4-byte aligned");
+    const Range rXh = rng(Xh, ((size_t)(n_slices) * g.Nc * g.Nc - 1) * ld_xh * sizeof(float) + n_bins * sizeof(float));
+    if (overlap(rXh, rng(X, (size_t)Nx_of(g) * g.K * sizeof(float))) ||
+        overlap(rXh, rng(D, (size_t)g.K * g.Nk * sizeof(float))))
+        return fail(HSNCT_E_ARG, "synthesize: Xh must not overlap X or D");
+    DeviceGuard guard(h->device);
+    CK(synthesize(g, X, D, slice0, n_slices, bin0, n_bins, Xh, ld_xh, (cudaStream_t)stream), "synthesize");
+    h->launches += 1;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int n_slices, int bin0,
+                       int n_bins, float* Xh, int64_t ld_xh, void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "dhr: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_window(g, slice0, n_slices, bin0, n_bins, ld_xh, "dhr");
+    if (st) return st;
+    if ((st = check_y(g, Y, ld_y, "dhr"))) return st;
+    if (n_slices == 0 || n_bins == 0) return HSNCT_OK;
+    if (!Xh || !aligned(Xh, 4)) return fail(HSNCT_E_ARG, "dhr: Xh is NULL or misaligned");
+    const size_t per = dhr_ws_per_slice(g);
+    if ((st = check_ws(ws, ws_bytes, a256(per), "dhr"))) return st;
+    const Range rXh = rng(Xh, ((size_t)(n_slices) * g.Nc * g.Nc - 1) * ld_xh * sizeof(float) + n_bins * sizeof(float));
+    if (overlap(rXh, rng(Y, (size_t)Np_of(g) * ld_y * sizeof(float))) || overlap(rXh, rng(ws, ws_bytes)))
+        return fail(HSNCT_E_ARG, "dhr: Xh must not overlap Y or the workspace");
+    DeviceGuard guard(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int kc = dhr_kc(g);
+    const int ns_pass = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_slices, ws_bytes / per));
+    float* Q = static_cast<float*>(ws);
+    for (int b = bin0; b < bin0 + n_bins; b += kc) {
+        const int nch = std::min(kc, bin0 + n_bins - b);
+        for (int r = slice0; r < slice0 + n_slices; r += ns_pass) {
+            const int ns = std::min(ns_pass, slice0 + n_slices - r);
+            CK(ramp_filter(g, h->t, Y + b, ld_y, nch, r, ns, Q, kc, s), "dhr ramp filter");
+            float* out = Xh + (int64_t)(r - slice0) * g.Nc * g.Nc * ld_xh;
+            CK(backproject(g, h->t, Q, kc, nch, r, ns, 1, out, ld_xh, b - bin0, s), "dhr backprojection");
+            h->launches += 2;
+        }
+    }
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
+                            const float* D0_host, int n_iter, float* Xh_host, float* V_host,
+                            float* D_host, void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fhr_host: handle is NULL");
+    const Geometry& g = h->g;
+    if (!Y_host || !V0_host || !D0_host || !Xh_host)
+        return fail(HSNCT_E_ARG, "fhr_host: Y, V0, D0 and Xh host buffers are required");
+    if (ld_y < g.Nk) return fail(HSNCT_E_ARG, "fhr_host: ld_y=%lld < N_k=%d", (long long)ld_y, g.Nk);
+    if (n_iter < 0) return fail(HSNCT_E_ARG, "fhr_host: n_iter=%d < 0", n_iter);
+    const FhrHostLayout L = fhr_layout(g, h->nmf);
+    hsnct_status st = check_ws(ws, ws_bytes, L.total, "fhr_host");
+    if (st) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    char* c = static_cast<char*>(ws);
+    float* Yd = (float*)c;
+    c += L.y;
+    float* Vd = (float*)c;
+    c += L.v;
+    float* Dd = (float*)c;
+    c += L.d;
+    float* Xd = (float*)c;
+    c += L.x;
+    float* Xhd = (float*)c;
+    c += L.xh;
+    void* wn = c;
+    c += L.nmf;
+    void* wf = c;
+    const int64_t Np = Np_of(g);
+    CK(cudaMemcpy2DAsync(Yd, (size_t)L.Nkp * sizeof(float), Y_host, (size_t)ld_y * sizeof(float),
+                         (size_t)g.Nk * sizeof(float), (size_t)Np, cudaMemcpyHostToDevice, s),
+       "fhr_host H2D Y");
+    CK(cudaMemcpyAsync(Vd, V0_host, (size_t)Np * g.K * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_host H2D V0");
+    CK(cudaMemcpyAsync(Dd, D0_host, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_host H2D D0");
+    if ((st = run_decompose(h, Yd, L.Nkp, Vd, Dd, n_iter, nullptr, wn, s))) return st;
+    if ((st = run_fbp(h, Vd, Xd, wf, s))) return st;
+    const int64_t wsl = fhr_window_slices(g);
+    const size_t slice_elems = (size_t)g.Nc * g.Nc * g.Nk;
+    for (int64_t r = 0; r < g.Nr; r += wsl) {
+        const int ns = (int)std::min<int64_t>(wsl, g.Nr - r);
+        CK(synthesize(g, Xd, Dd, (int)r, ns, 0, g.Nk, Xhd, g.Nk, s), "fhr_host synthesize");
+        h->launches += 1;
+        CK(cudaMemcpyAsync(Xh_host + (size_t)r * slice_elems, Xhd, (size_t)ns * slice_elems * sizeof(float),
+                           cudaMemcpyDeviceToHost, s),
+           "fhr_host D2H Xh");
+    }
+    if (V_host)
+        CK(cudaMemcpyAsync(V_host, Vd, (size_t)Np * g.K * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_host D2H V");
+    if (D_host)
+        CK(cudaMemcpyAsync(D_host, Dd, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_host D2H D");
+    return read_status(h, s);
+}
+
+hsnct_status hsnct_sync(hsnct_t h, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "sync: handle is NULL");
+    DeviceGuard guard(h->device);
+    return read_status(h, (cudaStream_t)stream);
+}
+
+uint64_t hsnct_kernel_launches(hsnct_t h) { return h ? h->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Internal declarations shared by the C ABI (api.cpp) and the CUDA kernels.
+// Nothing here is exported; the public surface is include/hsnct.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+namespace hsnct {
+
+// Device status word bits (deferred errors, read back by hsnct_sync).
+enum : unsigned {
+    ST_Y_NONFINITE = 1u,     // E_DATA
+    ST_Y_ALLZERO = 2u,       // E_DATA
+    ST_INIT_BAD = 4u,        // E_DATA: V0/D0 non-finite or negative
+    ST_NUMERIC = 8u,         // E_NUMERIC: V or D became non-finite
+};
+
+struct Geometry {
+    int Nv, Nr, Nc, Nk, K;
+    int P;       // FFT length = next_pow2(2 Nc)
+    int logP;
+    int num_sms; // SMs of the handle's device
+};
+
+// Per-handle device constants (small, owned by the handle).
+struct DeviceTables {
+    float* cos_t = nullptr;     // [Nv]
+    float* sin_t = nullptr;     // [Nv]
+    float* Hhat = nullptr;      // [P] real, even DFT of the zero-padded ramp kernel, / P folded in
+    float2* twiddle = nullptr;  // [P/2] exp(-2 pi i t / P)
+    unsigned* status = nullptr; // device status word
+    unsigned* counter = nullptr;// grid "last block" tickets (zero between launches)
+};
+
+// ---------------------------------------------------------------- NMF (nmf.cu)
+struct NmfPlan {
+    int nblk_v;      // blocks of the row pass
+    int nchunk;      // row chunks of the column pass
+    int64_t rows_per_chunk;
+    int bthreads;    // threads per column-pass block (one lambda-quad each)
+    int nlam_blk;    // lambda blocks of the column pass
+    int nblk_d;      // blocks of the D update
+    int Nkp;         // Nk rounded up to 4
+    size_t smem_v;   // dynamic smem of the row pass
+};
+struct NmfWs {
+    double* Gd;      // [K*K]   G = D D^T used by the current V half-step
+    double* vpart;   // [nblk_v*2]  per-block <V_new, A>, ||Y+||^2
+    double* dpart;   // [nblk_d]    per-block <B, D_new>
+    double* Gpart;   // [nblk_d*K*K] per-block partials of D_new D_new^T
+    double* ysq;     // [1]
+    double* Hpart;   // [nchunk*K*K]
+    float* Bpart;    // [nchunk*K*Nkp]
+};
+NmfPlan nmf_plan(const Geometry& g, int num_sms);
+size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);
+NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws);
+// Enqueues G = D D^T for the initial D (1 launch).
+cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* D,
+                            unsigned* status, cudaStream_t s);
+// Enqueues one Lee-Seung iteration (3 launches).
+cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
+                            int64_t ld_y, float* V, float* D, bool first, double* obj2,
+                            unsigned* status, unsigned* counter, cudaStream_t s);
+constexpr int NMF_LAUNCHES_PER_ITER = 3;
+
+// ------------------------------------------------------------- FBP (fbp.cu)
+// Ramp filter of Nch channels of every (v, r) sinogram row of the slice window
+// [s0, s0+ns):  element (v, r, c, ch) is in[((v*Nr + r)*Nc + c)*ld_in + ch].
+// Output Q[(r-s0)][v][c][Kc] (Kc >= Nch; channels >= Nch are written as 0).
+cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* in, int64_t ld_in,
+                        int Nch, int s0, int ns, float* Q, int Kc, cudaStream_t s);
+// Backprojection of Q[(r-s0)][v][c][Kc] for slices [s0, s0+ns).
+// mode 0 (FHR): X[ch][r][i][j] for ch < Nch (channel-planar, plane stride Nx).
+// mode 1 (DHR): Xh[((r-s0)*Nc + i)*Nc + j][ld_out] columns col0 + ch, ch < Nch.
+cudaError_t backproject(const Geometry& g, const DeviceTables& t, const float* Q, int Kc, int Nch,
+                        int s0, int ns, int mode, float* out, int64_t ld_out, int64_t col0,
+                        cudaStream_t s);
+int ramp_launches();
+int backproject_launches();
+
+// ------------------------------------------------------- synthesis (synth.cu)
+cudaError_t synthesize(const Geometry& g, const float* X, const float* D, int s0, int ns, int b0,
+                       int nb, float* Xh, int64_t ld_xh, cudaStream_t s);
+
+}  // namespace hsnct

@@ -1,0 +1,236 @@
+"""Thin Python binding of libhsnct.so (include/hsnct.h) -- argument marshalling only.
+
+PyTorch provides device memory and the current CUDA stream; every step of the
+hot path runs in the library's CUDA kernels.  There is no CPU fallback: if the
+shared library is missing or no CUDA device is present, construction raises.
+Method names follow the C ABI (hsnct_subspace_decompose -> subspace_decompose).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhsnct.so")
+
+OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
+OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST = range(4)
+MAX_SUB = 16
+
+_lock = threading.Lock()
+_lib = None
+
+
+class HsnctError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+
+
+class _Geom(ctypes.Structure):
+    _fields_ = [("n_views", ctypes.c_int32), ("n_rows", ctypes.c_int32),
+                ("n_cols", ctypes.c_int32), ("n_bins", ctypes.c_int32),
+                ("n_sub", ctypes.c_int32), ("angles", ctypes.POINTER(ctypes.c_double))]
+
+
+def lib():
+    """Load libhsnct.so (fails loudly if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                  "(nvcc, sm_100a); there is no CPU fallback")
+            L = ctypes.CDLL(LIB_PATH)
+            vp, i64, i32, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+            L.hsnct_create.argtypes = [ctypes.POINTER(_Geom), i32, ctypes.POINTER(vp)]
+            L.hsnct_create.restype = i32
+            L.hsnct_destroy.argtypes = [vp]
+            L.hsnct_destroy.restype = None
+            L.hsnct_workspace_bytes.argtypes = [vp, i32]
+            L.hsnct_workspace_bytes.restype = sz
+            L.hsnct_subspace_decompose.argtypes = [vp, vp, i64, vp, vp, i32, vp, vp, sz, vp]
+            L.hsnct_subspace_decompose.restype = i32
+            L.hsnct_fbp.argtypes = [vp, vp, vp, vp, sz, vp]
+            L.hsnct_fbp.restype = i32
+            L.hsnct_synthesize.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, i64, vp]
+            L.hsnct_synthesize.restype = i32
+            L.hsnct_dhr.argtypes = [vp, vp, i64, i32, i32, i32, i32, vp, i64, vp, sz, vp]
+            L.hsnct_dhr.restype = i32
+            L.hsnct_fhr_host.argtypes = [vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, sz, vp]
+            L.hsnct_fhr_host.restype = i32
+            L.hsnct_sync.argtypes = [vp, vp]
+            L.hsnct_sync.restype = i32
+            L.hsnct_kernel_launches.argtypes = [vp]
+            L.hsnct_kernel_launches.restype = ctypes.c_uint64
+            L.hsnct_status_string.argtypes = [i32]
+            L.hsnct_status_string.restype = ctypes.c_char_p
+            L.hsnct_last_error.argtypes = []
+            L.hsnct_last_error.restype = ctypes.c_char_p
+            L.hsnct_abi_version.argtypes = []
+            L.hsnct_abi_version.restype = i32
+            _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != OK:
+        L = lib()
+        raise HsnctError(st, f"{L.hsnct_status_string(st).decode()}: {L.hsnct_last_error().decode()}")
+
+
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream, device):
+    s = torch.cuda.current_stream(device) if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Hsnct:
+    """One handle per geometry (N_v, N_r, N_c, N_k, K) and device."""
+
+    def __init__(self, n_views, n_rows, n_cols, n_bins, n_sub, angles=None, device=0):
+        if not torch.cuda.is_available():
+            raise HsnctError(E_CUDA, "no CUDA device: the hot path has no CPU fallback")
+        self.device = torch.device("cuda", device if isinstance(device, int) else torch.device(device).index or 0)
+        self.Nv, self.Nr, self.Nc, self.Nk, self.K = n_views, n_rows, n_cols, n_bins, n_sub
+        self.Np = n_views * n_rows * n_cols
+        self.Nx = n_rows * n_cols * n_cols
+        L = lib()
+        self._angles = None
+        ap = None
+        if angles is not None:
+            import numpy as np
+            self._angles = np.ascontiguousarray(angles, dtype=np.float64)
+            ap = self._angles.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        g = _Geom(n_views, n_rows, n_cols, n_bins, n_sub, ap)
+        h = ctypes.c_void_p()
+        _check(L.hsnct_create(ctypes.byref(g), self.device.index, ctypes.byref(h)))
+        self._h = h
+        self._ws = {}
+
+    # -- lifetime -----------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hsnct_destroy(self._h)
+            self._h = None
+            self._ws.clear()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(lib().hsnct_kernel_launches(self._h))
+
+    def workspace_bytes(self, op: int) -> int:
+        return int(lib().hsnct_workspace_bytes(self._h, op))
+
+    def workspace(self, op: int, nbytes: int | None = None) -> torch.Tensor:
+        need = self.workspace_bytes(op) if nbytes is None else nbytes
+        ws = self._ws.get(op)
+        if ws is None or ws.numel() < need:
+            ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self._ws[op] = ws
+        return ws
+
+    # -- checks ---------------------------------------------------------------------
+    def _dev(self, t, name, shape=None, contiguous=True):
+        if not isinstance(t, torch.Tensor) or t.device != self.device or t.dtype != torch.float32:
+            raise HsnctError(E_ARG, f"{name} must be a float32 tensor on {self.device}")
+        if shape is not None and tuple(t.shape) != tuple(shape):
+            raise HsnctError(E_ARG, f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+        if contiguous and not t.is_contiguous():
+            raise HsnctError(E_ARG, f"{name} must be contiguous")
+        return t
+
+    def _rows(self, t, name, nrows, ncols):
+        self._dev(t, name, contiguous=False)
+        if t.dim() != 2 or t.shape[0] != nrows or t.shape[1] != ncols or t.stride(1) != 1:
+            raise HsnctError(E_ARG, f"{name} must be [{nrows}, {ncols}] with unit column stride")
+        return t.stride(0)
+
+    # -- the C ABI calls ------------------------------------------------------------
+    def subspace_decompose(self, Y, V, D, n_iter, obj_trace=None, ws=None, stream=None):
+        """Eq. 4 by Lee-Seung MU; V, D updated in place (hsnct_subspace_decompose)."""
+        ld = self._rows(Y, "Y", self.Np, self.Nk)
+        self._dev(V, "V", (self.Np, self.K))
+        self._dev(D, "D", (self.K, self.Nk))
+        if obj_trace is not None and (obj_trace.dtype != torch.float64 or obj_trace.device != self.device
+                                      or obj_trace.numel() < 2 * n_iter or not obj_trace.is_contiguous()):
+            raise HsnctError(E_ARG, "obj_trace must be a contiguous float64 device tensor of 2*n_iter")
+        ws = self.workspace(OP_DECOMPOSE) if ws is None else ws
+        _check(lib().hsnct_subspace_decompose(self._h, _ptr(Y), ld, _ptr(V), _ptr(D), int(n_iter),
+                                              _ptr(obj_trace), _ptr(ws), ws.numel() * ws.element_size(),
+                                              _stream(stream, self.device)))
+        return V, D
+
+    def fbp(self, V, X=None, ws=None, stream=None):
+        """FBP of the K subspace sinograms -> X [K, N_r, N_c, N_c] (hsnct_fbp)."""
+        self._dev(V, "V", (self.Np, self.K))
+        if X is None:
+            X = torch.empty((self.K, self.Nr, self.Nc, self.Nc), dtype=torch.float32, device=self.device)
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        ws = self.workspace(OP_FBP) if ws is None else ws
+        _check(lib().hsnct_fbp(self._h, _ptr(V), _ptr(X), _ptr(ws), ws.numel() * ws.element_size(),
+                               _stream(stream, self.device)))
+        return X
+
+    def synthesize(self, X, D, slice0=0, n_slices=None, bin0=0, n_bins=None, Xh=None, stream=None):
+        """x^h window = x^s (D^s)^T (hsnct_synthesize) -> Xh [n_slices*N_c^2, n_bins]."""
+        n_slices = self.Nr - slice0 if n_slices is None else n_slices
+        n_bins = self.Nk - bin0 if n_bins is None else n_bins
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        self._dev(D, "D", (self.K, self.Nk))
+        if Xh is None:
+            Xh = torch.empty((n_slices * self.Nc * self.Nc, n_bins), dtype=torch.float32, device=self.device)
+        ld = self._rows(Xh, "Xh", n_slices * self.Nc * self.Nc, n_bins) if Xh.numel() else max(n_bins, 1)
+        _check(lib().hsnct_synthesize(self._h, _ptr(X), _ptr(D), slice0, n_slices, bin0, n_bins,
+                                      _ptr(Xh), ld, _stream(stream, self.device)))
+        return Xh
+
+    def dhr(self, Y, slice0=0, n_slices=None, bin0=0, n_bins=None, Xh=None, ws=None, stream=None):
+        """Per-bin FBP baseline (hsnct_dhr) -> Xh [n_slices*N_c^2, n_bins]."""
+        n_slices = self.Nr - slice0 if n_slices is None else n_slices
+        n_bins = self.Nk - bin0 if n_bins is None else n_bins
+        ld_y = self._rows(Y, "Y", self.Np, self.Nk)
+        if Xh is None:
+            Xh = torch.empty((n_slices * self.Nc * self.Nc, n_bins), dtype=torch.float32, device=self.device)
+        ld = self._rows(Xh, "Xh", n_slices * self.Nc * self.Nc, n_bins) if Xh.numel() else max(n_bins, 1)
+        if ws is None:
+            per = self.workspace_bytes(OP_DHR)
+            ws = self.workspace(OP_DHR, per * max(1, min(n_slices, 64)))
+        _check(lib().hsnct_dhr(self._h, _ptr(Y), ld_y, slice0, n_slices, bin0, n_bins, _ptr(Xh), ld,
+                               _ptr(ws), ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        return Xh
+
+    def fhr_host(self, Y, V0, D0, n_iter, Xh=None, V=None, D=None, ws=None, stream=None):
+        """Algorithm 1 end to end on HOST tensors (hsnct_fhr_host); blocks until Xh is on the host."""
+        for t, name in ((Y, "Y"), (V0, "V0"), (D0, "D0")):
+            if t.device.type != "cpu" or t.dtype != torch.float32:
+                raise HsnctError(E_ARG, f"{name} must be a float32 host tensor")
+        if Y.dim() != 2 or Y.shape != (self.Np, self.Nk) or Y.stride(1) != 1:
+            raise HsnctError(E_ARG, "Y must be [N_p, N_k] with unit column stride")
+        V0 = V0.contiguous()
+        D0 = D0.contiguous()
+        if Xh is None:
+            Xh = torch.empty((self.Nx, self.Nk), dtype=torch.float32, pin_memory=True)
+        if not Xh.is_contiguous() or Xh.shape != (self.Nx, self.Nk):
+            raise HsnctError(E_ARG, "Xh must be a contiguous [N_x, N_k] host tensor")
+        ws = self.workspace(OP_FHR_HOST) if ws is None else ws
+        _check(lib().hsnct_fhr_host(self._h, _ptr(Y), Y.stride(0), _ptr(V0), _ptr(D0), int(n_iter),
+                                    _ptr(Xh), _ptr(V), _ptr(D), _ptr(ws), ws.numel() * ws.element_size(),
+                                    _stream(stream, self.device)))
+        return Xh
+
+    def sync(self, stream=None):
+        """Wait for the stream; raise the deferred data/numeric status (hsnct_sync)."""
+        _check(lib().hsnct_sync(self._h, _stream(stream, self.device)))

@@ -1,0 +1,331 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle on the same
+seeded inputs.  Tolerances (BASELINE.json north_star):
+  FBP and synthesis  <= 1e-4 relative L2;
+  NMF (fixed init, fixed iteration count) <= 1e-3 relative L2 on V, D and x^h.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthdata as sd
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda:0")
+
+
+def rel(a, b):
+    a = a.detach().cpu().double().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, np.float64)
+    b = b.detach().cpu().double().numpy() if isinstance(b, torch.Tensor) else np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def H():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2410_22500_b200 import Hsnct, lib
+    lib()
+
+    def make(cfg, angles=None):
+        return Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, angles=angles, device=0)
+    return make
+
+
+def padded(Y, ld, fill=float("nan")):
+    """Y on the device with ld >= Nk, padding columns poisoned (must be ignored)."""
+    Np, Nk = Y.shape
+    buf = torch.full((Np, ld), fill, dtype=torch.float32, device=DEV)
+    buf[:, :Nk] = Y.to(DEV)
+    return buf[:, :Nk]
+
+
+# ---------------------------------------------------------------------- NMF
+@pytest.mark.parametrize("cfg,n_iter", [
+    (sd.CONFIGS[1], 100),
+    (sd.custom(idx=7, Nc=20, Nv=13, Nk=203, K=5, M=4), 40),     # ragged N_p, N_k % 4 != 0
+    (sd.custom(idx=8, Nc=17, Nv=9, Nk=37, K=1, M=2), 30),       # K = 1
+    (sd.custom(idx=9, Nc=24, Nv=10, Nr=3, Nk=64, K=16, M=5), 25),  # K = 16, several slices
+])
+def test_nmf_parity(H, cfg, n_iter):
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    Yd = padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4 + 4)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    obj = torch.zeros(2 * n_iter, dtype=torch.float64, device=DEV)
+    h.subspace_decompose(Yd, V, D, n_iter, obj_trace=obj)
+    h.sync()
+    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter, objective=True)
+    assert rel(V, Vo) <= 1e-3, rel(V, Vo)
+    assert rel(D, Do) <= 1e-3, rel(D, Do)
+    ob = obj.cpu().numpy()
+    np.testing.assert_allclose(ob, objo, rtol=1e-3)
+    assert np.all(np.diff(ob) <= 1e-5 * np.abs(ob[:-1]))
+
+
+def test_nmf_parity_c2_shape(H):
+    cfg = sd.CONFIGS[2]
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    n = 12
+    h.subspace_decompose(pr["Y"].to(DEV), V, D, n)
+    h.sync()
+    Vo, Do = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n)
+    assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
+
+
+def test_nmf_deterministic_and_resumable(H):
+    cfg = sd.CONFIGS[1]
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    Y = pr["Y"].to(DEV)
+    outs = []
+    for split in ((30,), (30,), (11, 19)):
+        V = pr["V0"].to(DEV).clone()
+        D = pr["D0"].to(DEV).clone()
+        for n in split:
+            h.subspace_decompose(Y, V, D, n)
+        h.sync()
+        outs.append((V.cpu(), D.cpu()))
+    for V, D in outs[1:]:
+        assert torch.equal(V, outs[0][0]) and torch.equal(D, outs[0][1])
+
+
+def test_nmf_fixed_point(H):
+    cfg = sd.custom(idx=10, Nc=16, Nv=8, Nk=24, K=3)
+    h = H(cfg)
+    g = torch.Generator().manual_seed(3)
+    Vs = torch.randint(1, 5, (cfg.Np, 3), generator=g).float()
+    Ds = torch.randint(1, 5, (3, cfg.Nk), generator=g).float()
+    Y = (Vs @ Ds).to(DEV)
+    V, D = Vs.to(DEV).clone(), Ds.to(DEV).clone()
+    h.subspace_decompose(Y, V, D, 10)
+    h.sync()
+    assert rel(V, Vs) < 1e-6 and rel(D, Ds) < 1e-6
+
+
+def test_nmf_zero_iterations_noop(H):
+    cfg = sd.CONFIGS[1]
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(pr["Y"].to(DEV), V, D, 0)
+    h.sync()
+    assert torch.equal(V.cpu(), pr["V0"]) and torch.equal(D.cpu(), pr["D0"])
+
+
+# ---------------------------------------------------------------------- FBP
+@pytest.mark.parametrize("cfg", [
+    sd.CONFIGS[1],
+    sd.custom(idx=11, Nc=63, Nv=37, Nr=2, Nk=10, K=5),
+    sd.custom(idx=12, Nc=100, Nv=45, Nr=1, Nk=20, K=16),
+    sd.custom(idx=13, Nc=33, Nv=8, Nr=3, Nk=4, K=1),
+])
+def test_fbp_parity(H, cfg):
+    g = torch.Generator().manual_seed(cfg.idx)
+    V = torch.rand((cfg.Np, cfg.K), generator=g)
+    h = H(cfg)
+    X = h.fbp(V.to(DEV))
+    torch.cuda.synchronize()
+    Xo = oracle.fbp(V.numpy(), cfg.Nv, cfg.Nr, cfg.Nc)
+    assert rel(X, Xo) <= 1e-4, rel(X, Xo)
+
+
+def test_fbp_custom_angles(H):
+    cfg = sd.custom(idx=14, Nc=40, Nv=17, Nk=6, K=3)
+    ang = np.sort(np.random.default_rng(2).uniform(0, math.pi, cfg.Nv))
+    V = torch.rand((cfg.Np, cfg.K), generator=torch.Generator().manual_seed(1))
+    h = H(cfg, angles=ang)
+    X = h.fbp(V.to(DEV))
+    torch.cuda.synchronize()
+    Xo = oracle.fbp(V.numpy(), cfg.Nv, cfg.Nr, cfg.Nc, angles=ang)
+    assert rel(X, Xo) <= 1e-4
+
+
+def test_fbp_single_view_impulse_pin(H):
+    """Closed form: one impulse at theta = 0 gives (pi/Nv) h[j - c0] in every row."""
+    cfg = sd.custom(idx=15, Nc=32, Nv=6, Nk=1, K=1)
+    V = torch.zeros((cfg.Np, 1))
+    c0 = 9
+    V[c0, 0] = 1.0  # view 0, row 0, column c0
+    h = H(cfg)
+    X = h.fbp(V.to(DEV)).cpu()[0, 0].double().numpy()
+    hk = np.array([oracle.ramp_kernel(j - c0) for j in range(cfg.Nc)])
+    np.testing.assert_allclose(X, np.tile(math.pi / cfg.Nv * hk, (cfg.Nc, 1)), atol=2e-7)
+
+
+def test_fbp_analytic_disk(H):
+    Nc, Nv = 256, 180
+    cfg = sd.custom(idx=16, Nc=Nc, Nv=Nv, Nk=1, K=1)
+    th = torch.as_tensor(sd.view_angles(Nv), dtype=torch.float64)[:, None]
+    t = (torch.arange(Nc, dtype=torch.float64) - 0.5 * (Nc - 1))[None, :]
+    P = sd.ellipse_line_integrals(th, t, 0.0, 0.0, 0.3 * Nc, 0.3 * Nc, 0.0)
+    h = H(cfg)
+    X = h.fbp(P.float().reshape(-1, 1).to(DEV)).cpu()[0, 0].double().numpy()
+    yy, xx = np.mgrid[0:Nc, 0:Nc] - 0.5 * (Nc - 1)
+    assert X[np.hypot(xx, yy) < 0.24 * Nc].mean() == pytest.approx(1.0, abs=3e-3)
+
+
+# ---------------------------------------------------------------- synthesis
+@pytest.mark.parametrize("window", [(0, None, 0, None), (1, 2, 3, 17), (2, 1, 5, 3)])
+def test_synthesize_parity(H, window):
+    cfg = sd.custom(idx=17, Nc=12, Nv=5, Nr=4, Nk=41, K=6)
+    g = torch.Generator().manual_seed(4)
+    X = torch.randn((cfg.K, cfg.Nr, cfg.Nc, cfg.Nc), generator=g)
+    D = torch.rand((cfg.K, cfg.Nk), generator=g)
+    s0, ns, b0, nb = window
+    ns = cfg.Nr - s0 if ns is None else ns
+    nb = cfg.Nk - b0 if nb is None else nb
+    h = H(cfg)
+    Xh = h.synthesize(X.to(DEV), D.to(DEV), s0, ns, b0, nb)
+    torch.cuda.synchronize()
+    Xo = oracle.synthesize(X.numpy(), D.numpy(), s0, ns, b0, nb)
+    assert rel(Xh, Xo) <= 1e-6
+
+
+def test_synthesize_strided_unaligned_output(H):
+    cfg = sd.custom(idx=18, Nc=8, Nv=5, Nr=2, Nk=30, K=4)
+    g = torch.Generator().manual_seed(5)
+    X = torch.randn((cfg.K, cfg.Nr, cfg.Nc, cfg.Nc), generator=g).to(DEV)
+    D = torch.rand((cfg.K, cfg.Nk), generator=g).to(DEV)
+    big = torch.full((cfg.Nx, 33), -7.0, device=DEV)
+    out = big[:, 1:1 + 29]            # ld = 33, misaligned base
+    h = H(cfg)
+    h.synthesize(X, D, 0, cfg.Nr, 1, 29, Xh=out)
+    torch.cuda.synchronize()
+    Xo = oracle.synthesize(X.cpu().numpy(), D.cpu().numpy(), 0, cfg.Nr, 1, 29)
+    assert rel(out, Xo) <= 1e-6
+    assert torch.all(big[:, 0] == -7.0) and torch.all(big[:, 30:] == -7.0)
+
+
+def test_synthesize_empty_window(H):
+    cfg = sd.custom(idx=19, Nc=8, Nv=5, Nr=2, Nk=30, K=4)
+    h = H(cfg)
+    X = torch.zeros((cfg.K, cfg.Nr, cfg.Nc, cfg.Nc), device=DEV)
+    D = torch.zeros((cfg.K, cfg.Nk), device=DEV)
+    out = h.synthesize(X, D, 1, 0, 0, 5)
+    assert out.numel() == 0
+
+
+# ---------------------------------------------------------------------- DHR
+@pytest.mark.parametrize("cfg,window", [
+    (sd.CONFIGS[1], (0, 1, 0, 40)),
+    (sd.custom(idx=20, Nc=50, Nv=21, Nr=3, Nk=37, K=2), (1, 2, 3, 33)),
+])
+def test_dhr_parity(H, cfg, window):
+    pr = sd.make_problem(cfg)
+    s0, ns, b0, nb = window
+    h = H(cfg)
+    Xh = h.dhr(pr["Y"].to(DEV), s0, ns, b0, nb)
+    torch.cuda.synchronize()
+    Xo = oracle.dhr(pr["Y"].numpy(), cfg.Nv, cfg.Nr, cfg.Nc, slice0=s0, n_slices=ns, bin0=b0, n_bins=nb)
+    assert rel(Xh, Xo) <= 1e-4, rel(Xh, Xo)
+
+
+def test_linearity_identity_on_gpu(H):
+    """Y = V D exactly: fbp + synthesize == dhr."""
+    cfg = sd.custom(idx=21, Nc=40, Nv=30, Nr=2, Nk=23, K=3)
+    g = torch.Generator().manual_seed(6)
+    V = torch.randint(0, 8, (cfg.Np, cfg.K), generator=g).float()
+    D = torch.randint(0, 8, (cfg.K, cfg.Nk), generator=g).float() / 4
+    Y = (V.double() @ D.double()).float()
+    h = H(cfg)
+    X = h.fbp(V.to(DEV))
+    a = h.synthesize(X, D.to(DEV))
+    b = h.dhr(Y.to(DEV))
+    torch.cuda.synchronize()
+    assert rel(a, b) <= 1e-5
+
+
+# ------------------------------------------------------------ whole pipeline
+@pytest.mark.parametrize("cfgi,n_iter", [(1, 100), (2, 8)])
+def test_fhr_pipeline_parity(H, cfgi, n_iter):
+    cfg = sd.CONFIGS[cfgi]
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(pr["Y"].to(DEV), V, D, n_iter)
+    X = h.fbp(V)
+    Xh = h.synthesize(X, D)
+    h.sync()
+    Vo, Do = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter)
+    Xo = oracle.fbp(Vo, cfg.Nv, cfg.Nr, cfg.Nc)
+    Xho = oracle.synthesize(Xo, Do)
+    assert rel(Xh, Xho) <= 1e-3, rel(Xh, Xho)
+
+
+def test_fhr_host_matches_device_path(H):
+    cfg = sd.CONFIGS[1]
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    n = 25
+    Vh = torch.empty_like(pr["V0"])
+    Dh = torch.empty_like(pr["D0"])
+    Xh_host = h.fhr_host(pr["Y"].pin_memory(), pr["V0"], pr["D0"], n, V=Vh, D=Dh)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(pr["Y"].to(DEV), V, D, n)
+    Xh = h.synthesize(h.fbp(V), D)
+    h.sync()
+    assert torch.equal(Vh, V.cpu()) and torch.equal(Dh, D.cpu())
+    assert torch.equal(Xh_host, Xh.cpu())
+
+
+# ----------------------------------------------------------------- errors
+def test_deferred_data_errors(H):
+    from paper_2410_22500_b200 import HsnctError
+    cfg = sd.custom(idx=22, Nc=16, Nv=8, Nk=12, K=2)
+    h = H(cfg)
+    Y = torch.rand((cfg.Np, cfg.Nk), device=DEV)
+    V = torch.rand((cfg.Np, 2), device=DEV) + 0.1
+    D = torch.rand((2, cfg.Nk), device=DEV) + 0.1
+    Y[3, 4] = float("nan")
+    h.subspace_decompose(Y, V.clone(), D.clone(), 2)
+    with pytest.raises(HsnctError) as e:
+        h.sync()
+    assert e.value.status == 2
+    h.sync()  # cleared
+    h.subspace_decompose(-torch.rand((cfg.Np, cfg.Nk), device=DEV), V.clone(), D.clone(), 2)
+    with pytest.raises(HsnctError) as e:
+        h.sync()
+    assert e.value.status == 2
+    Dn = D.clone()
+    Dn[0, 0] = -1.0
+    h.subspace_decompose(torch.rand((cfg.Np, cfg.Nk), device=DEV), V.clone(), Dn, 1)
+    with pytest.raises(HsnctError) as e:
+        h.sync()
+    assert e.value.status == 2
+
+
+def test_argument_errors(H):
+    from paper_2410_22500_b200 import HsnctError
+    cfg = sd.custom(idx=23, Nc=16, Nv=8, Nk=12, K=2)
+    h = H(cfg)
+    Y = torch.rand((cfg.Np, cfg.Nk), device=DEV)
+    V = torch.rand((cfg.Np, 2), device=DEV)
+    D = torch.rand((2, cfg.Nk), device=DEV)
+    with pytest.raises(HsnctError):
+        h.subspace_decompose(Y, V, D, -1)
+    small = torch.empty(8, dtype=torch.uint8, device=DEV)
+    with pytest.raises(HsnctError) as e:
+        h.subspace_decompose(Y, V, D, 1, ws=small)
+    assert e.value.status == 1
+    with pytest.raises(HsnctError):
+        h.synthesize(torch.zeros((2, 1, 16, 16), device=DEV), D, 0, 2, 0, 12)
+    Ybig = torch.rand((cfg.Np, 13), device=DEV)[:, 1:]   # misaligned base
+    with pytest.raises(HsnctError):
+        h.subspace_decompose(Ybig, V, D, 1)
+    import ctypes
+    from paper_2410_22500_b200 import hsnct as hm
+    ws = h.workspace(hm.OP_DECOMPOSE)
+    st = hm.lib().hsnct_subspace_decompose(h._h, ctypes.c_void_p(Y.data_ptr()), 12,
+                                           ctypes.c_void_p(Y.data_ptr()), ctypes.c_void_p(D.data_ptr()),
+                                           1, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), None)
+    assert st == 1 and b"overlap" in hm.lib().hsnct_last_error()
