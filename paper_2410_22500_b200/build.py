@@ -18,7 +18,7 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhsnct.so")
 BUILD = os.path.join(HERE, "build")
 
-SOURCES = ["api.cpp", "nmf.cu", "fbp.cu", "synth.cu"]
+SOURCES = ["api.cpp", "nmf.cu", "nmf_fused.cu", "fbp.cu", "synth.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{INC}", f"-I{CSRC}"]

@@ -35,36 +35,59 @@ struct DeviceTables {
 };
 
 // ---------------------------------------------------------------- NMF (nmf.cu)
+constexpr int DG2 = 8;  // chunk groups of the D-update reduction
 struct NmfPlan {
-    int nblk_v;      // blocks of the row pass
-    int nchunk;      // row chunks of the column pass
-    int64_t rows_per_chunk;
-    int bthreads;    // threads per column-pass block (one lambda-quad each)
-    int nlam_blk;    // lambda blocks of the column pass
-    int nblk_d;      // blocks of the D update
     int Nkp;         // Nk rounded up to 4
-    size_t smem_v;   // dynamic smem of the row pass
+    int nbx;         // D-update column blocks = ceil(Nk / 32)
+    int P;           // number of per-CTA B partials
+    int PH;          // number of per-CTA H partials
+    int nvp;         // number of per-CTA objective partials
+    // fused single-pass path (nmf_fused.cu), K <= 8
+    bool fused;
+    int LP;          // lambda pairs per thread
+    int nbuf;        // tile ring depth
+    int PB;          // B partials of the fused kernel (2 per CTA)
+    int nby;         // blocks of the Y+ preparation kernel
+    int fthreads;    // threads per CTA
+    int nblk_f;      // CTAs (persistent, static tile schedule)
+    size_t smem_f;   // dynamic smem (tile ring)
+    // two-pass fallback (nmf.cu)
+    int nblk_v, nchunk, bthreads, nlam_blk;
+    int64_t rows_per_chunk;
+    size_t smem_v;
 };
 struct NmfWs {
     double* Gd;      // [K*K]   G = D D^T used by the current V half-step
-    double* vpart;   // [nblk_v*2]  per-block <V_new, A>, ||Y+||^2
-    double* dpart;   // [nblk_d]    per-block <B, D_new>
-    double* Gpart;   // [nblk_d*K*K] per-block partials of D_new D_new^T
+    double* vpart;   // [nvp*2] per-CTA <V_new, A>, ||Y+||^2
+    double* dpart;   // [nbx]   per-column <B, D_new>
+    double* Gpart;   // [nbx*K*K] per-column partials of D_new D_new^T
     double* ysq;     // [1]
-    double* Hpart;   // [nchunk*K*K]
-    float* Bpart;    // [nchunk*K*Nkp]
+    double* Hpart;   // [P*K*K]
+    float* Bpart;    // [P*K*Nkp]
+    double* L2B;     // [nbx*DG2*K*32]
+    double* L2H;     // [nbx*DG2*K*K]
+    float* Yp;       // [Np*Nkp] Y+ (fused path only)
+    double* ypart;   // [nby] ||Y+||^2 partials (fused path only)
 };
 NmfPlan nmf_plan(const Geometry& g, int num_sms);
+bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p);
 size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);
 NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws);
-// Enqueues G = D D^T for the initial D (1 launch).
-cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* D,
-                            unsigned* status, cudaStream_t s);
-// Enqueues one Lee-Seung iteration (3 launches).
+// Enqueues the per-call preparation: G = D D^T for the initial D, and Y+ for the
+// fused path (nmf_init_launches launches).
+cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                            const float* D, unsigned* status, cudaStream_t s);
+int nmf_init_launches(const NmfPlan& p);
+// Enqueues one Lee-Seung iteration (nmf_launches_per_iter launches).
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
                             int64_t ld_y, float* V, float* D, bool first, double* obj2,
                             unsigned* status, unsigned* counter, cudaStream_t s);
-constexpr int NMF_LAUNCHES_PER_ITER = 3;
+cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
+                             unsigned* status, cudaStream_t s);
+cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                             unsigned* status, cudaStream_t s);
+int nmf_launches_per_iter(const NmfPlan& p);
+// counter words needed by the handle: 1 + ceil(Nk / 32)
 
 // ------------------------------------------------------------- FBP (fbp.cu)
 // Ramp filter of Nch channels of every (v, r) sinogram row of the slice window

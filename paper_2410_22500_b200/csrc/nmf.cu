@@ -22,7 +22,6 @@ constexpr int VW = VT / 32;    // row-pass warps
 constexpr int RPW = 4;         // rows per warp step
 constexpr int BT_MAX = 128;    // column-pass threads (one lambda quad each)
 constexpr int BROWS = 32;      // V rows staged per column-pass sub-chunk
-constexpr int DT = 256;        // D-update threads (one lambda each)
 
 __device__ __forceinline__ float4 ld4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
@@ -63,31 +62,34 @@ __device__ __forceinline__ unsigned warp_or(unsigned v) {
 }
 
 // ------------------------------------------------------------------ G init
+// G = D0 D0^T (fp64), thread t -> output t % K^2, lambda residue class t / K^2,
+// classes combined in a fixed order.  Also validates D0 (finite, >= 0).
 template <int K>
 __global__ void __launch_bounds__(256) k_gram_init(const float* __restrict__ D, int Nk,
                                                    double* __restrict__ Gd,
                                                    unsigned* __restrict__ status) {
-    __shared__ double part[256];
+    constexpr int KK = K * K;
+    constexpr int NG = 256 / KK;
+    __shared__ double part[NG][KK];
     unsigned bad = 0;
     for (int i = threadIdx.x; i < K * Nk; i += blockDim.x) {
-        float d = D[i];
+        const float d = D[i];
         if (!(isfinite(d) && d >= 0.f)) bad = ST_INIT_BAD;
     }
     bad = warp_or(bad);
     if (bad && (threadIdx.x & 31) == 0) atomicOr(status, bad);
-    for (int t = 0; t < K * K; ++t) {
-        const int a = t / K, b = t % K;
+    if ((int)threadIdx.x < NG * KK) {
+        const int o = threadIdx.x % KK, gg = threadIdx.x / KK;
+        const int a = o / K, b = o - (o / K) * K;
         double s = 0.0;
-        for (int l = threadIdx.x; l < Nk; l += blockDim.x)
-            s += (double)D[(int64_t)a * Nk + l] * (double)D[(int64_t)b * Nk + l];
-        part[threadIdx.x] = s;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-            if ((int)threadIdx.x < w) part[threadIdx.x] += part[threadIdx.x + w];
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) Gd[t] = part[0];
-        __syncthreads();
+        for (int l = gg; l < Nk; l += NG) s = fma((double)D[(int64_t)a * Nk + l], (double)D[(int64_t)b * Nk + l], s);
+        part[gg][o] = s;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < KK) {
+        double s = 0.0;
+        for (int gg = 0; gg < NG; ++gg) s += part[gg][threadIdx.x];
+        Gd[threadIdx.x] = s;
     }
 }
 
@@ -231,12 +233,14 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
     const int l0 = q * 4;
     const int64_t rb0 = (int64_t)blockIdx.x * rpc;
     const int64_t re = min(Np, rb0 + rpc);
-    const bool do_h = blockIdx.y == 0 && tid < K * K;
-    const int ha = tid / K, hb = tid - (tid / K) * K;
+    constexpr int HPT = (K * K + 31) / 32;  // H outputs per thread (blockDim >= 32)
+    const bool do_h = blockIdx.y == 0;
     float4 acc[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    double h = 0.0;
+    double h[HPT];
+#pragma unroll
+    for (int j = 0; j < HPT; ++j) h[j] = 0.0;
     for (int64_t rb = rb0; rb < re; rb += BROWS) {
         const int nr = (int)min((int64_t)BROWS, re - rb);
         __syncthreads();
@@ -280,9 +284,16 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
             }
         }
         if (do_h) {
-            double hs = 0.0;
-            for (int i = 0; i < nr; ++i) hs = fma((double)Vs[i * K + ha], (double)Vs[i * K + hb], hs);
-            h += hs;
+#pragma unroll
+            for (int j = 0; j < HPT; ++j) {
+                const int t = tid + j * (int)blockDim.x;
+                if (t < K * K) {
+                    const int ha = t / K, hb = t - (t / K) * K;
+                    double hs = 0.0;
+                    for (int i = 0; i < nr; ++i) hs = fma((double)Vs[i * K + ha], (double)Vs[i * K + hb], hs);
+                    h[j] += hs;
+                }
+            }
         }
     }
     if (qv) {
@@ -290,115 +301,201 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
         for (int k = 0; k < K; ++k)
             reinterpret_cast<float4*>(Bpart + ((int64_t)blockIdx.x * K + k) * Nkp)[q] = acc[k];
     }
-    if (do_h) Hpart[(int64_t)blockIdx.x * K * K + tid] = h;
+    if (do_h) {
+#pragma unroll
+        for (int j = 0; j < HPT; ++j) {
+            const int t = tid + j * (int)blockDim.x;
+            if (t < K * K) Hpart[(int64_t)blockIdx.x * K * K + t] = h[j];
+        }
+    }
 }
 
-// ---------------------------------------------------------------- D update
+// Fixed-order block reduction of one double per thread (result valid in thread 0).
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+    return s;
+}
+
+// ------------------------------------------------------------- D update v2
+// Two-stage fixed-order reduction of the P per-CTA partials, spread over a
+// (ceil(N_k/32) x DG2) grid so that the reads of the partials are issued by
+// many SMs at once:
+//   block (bx, by): B partial sums for lambdas [32 bx, 32 bx + 32) over the chunks
+//                   c = by*8 + w (mod 8*DG2) (warp w), and an H partial over the
+//                   chunks c = by + DG2*m; written as level-2 partials.
+//   last of the DG2 blocks of column bx: B, H in a fixed order, D update for its
+//                   32 lambdas, <B, D_new> and (D_new D_new^T) partials.
+//   last column block overall: G for the next row pass and the objective terms.
 template <int K>
-__global__ void __launch_bounds__(DT) k_dupdate(const float* __restrict__ Bpart,
-                                                const double* __restrict__ Hpart, int nchunk, int Nk,
-                                                int Nkp, float* __restrict__ D, double* __restrict__ Gd,
-                                                const double* __restrict__ vpart, int nblk_v,
-                                                double* __restrict__ dpart, double* __restrict__ Gpart,
-                                                double* __restrict__ ysq_store, int first,
-                                                double* __restrict__ obj2,
-                                                unsigned* __restrict__ counter,
-                                                unsigned* __restrict__ status) {
-    __shared__ double Hs[K * K];
-    __shared__ double dsm[K][DT];
-    __shared__ double red[DT / 32];
-    __shared__ int is_last;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int t = tid; t < K * K; t += DT) {
+__global__ void __launch_bounds__(256) k_dred(const float* __restrict__ Bpart,
+                                              const double* __restrict__ Hpart, int P, int PH, int Nk, int Nkp,
+                                              float* __restrict__ D, double* __restrict__ Gd,
+                                              const double* __restrict__ vpart, int nblk_v,
+                                              const double* __restrict__ ypart, int nby,
+                                              double* __restrict__ L2B, double* __restrict__ L2H,
+                                              double* __restrict__ dpart, double* __restrict__ Gpart,
+                                              double* __restrict__ ysq_store, int first,
+                                              double* __restrict__ obj2,
+                                              unsigned* __restrict__ colcnt,
+                                              unsigned* __restrict__ counter,
+                                              unsigned* __restrict__ status) {
+    constexpr int KK = K * K;
+    constexpr int NS = (256 / KK) > 0 ? (256 / KK) : 1;
+    __shared__ double bw[8][K][32];
+    __shared__ double hs[NS][KK];
+    __shared__ double Hs[KK];
+    __shared__ double dsm[K][32];
+    __shared__ double red[8];
+    __shared__ double sc[4];
+    __shared__ int flag;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int bx = blockIdx.x, by = blockIdx.y, nbx = gridDim.x;
+    const int l = bx * 32 + lane;
+    // ---- stage A: level-2 partials
+    {
+        double acc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = 0.0;
+        if (l < Nk) {
+            for (int c = by * 8 + w; c < P; c += 8 * DG2) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) acc[k] += (double)__ldcg(Bpart + ((int64_t)c * K + k) * Nkp + l);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) bw[w][k][lane] = acc[k];
+    }
+    for (int t = tid; t < KK * NS; t += 256) {
+        const int o = t % KK, sub = t / KK;
         double s = 0.0;
-        for (int c = 0; c < nchunk; ++c) s += Hpart[(int64_t)c * K * K + t];
-        Hs[t] = s;
+        for (int c = by + DG2 * sub; c < PH; c += DG2 * NS) s += __ldcg(Hpart + (int64_t)c * KK + o);
+        hs[sub][o] = s;
     }
     __syncthreads();
-    const int l = blockIdx.x * DT + tid;
-    double bd = 0.0;
+    for (int t = tid; t < K * 32; t += 256) {
+        const int k = t / 32, ln = t % 32;
+        double s = 0.0;
+        for (int ww = 0; ww < 8; ++ww) s += bw[ww][k][ln];
+        L2B[(((int64_t)bx * DG2 + by) * K + k) * 32 + ln] = s;
+    }
+    for (int o = tid; o < KK; o += 256) {
+        double s = 0.0;
+        for (int sub = 0; sub < NS; ++sub) s += hs[sub][o];
+        L2H[((int64_t)bx * DG2 + by) * KK + o] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) flag = (atomicAdd(colcnt + bx, 1u) == DG2 - 1);
+    __syncthreads();
+    if (!flag) return;
+    __threadfence();
+    // ---- column finalize (last of the DG2 blocks of column bx)
+    for (int o = tid; o < KK; o += 256) {
+        double s = 0.0;
+        for (int yy = 0; yy < DG2; ++yy) s += __ldcg(L2H + ((int64_t)bx * DG2 + yy) * KK + o);
+        Hs[o] = s;
+    }
+    __syncthreads();
     unsigned bad = 0;
-    if (l < Nk) {
-        double B[K], d[K];
+    double bd = 0.0;
+    if (w == 0) {
+        if (l < Nk) {
+            double B[K], d[K];
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double s = 0.0;
-            for (int c = 0; c < nchunk; ++c) s += (double)Bpart[((int64_t)c * K + k) * Nkp + l];
-            B[k] = s;
-            d[k] = (double)D[(int64_t)k * Nk + l];
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int yy = 0; yy < DG2; ++yy) s += __ldcg(L2B + (((int64_t)bx * DG2 + yy) * K + k) * 32 + lane);
+                B[k] = s;
+                d[k] = (double)D[(int64_t)k * Nk + l];
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double hd = 0.0;
+#pragma unroll
+                for (int j = 0; j < K; ++j) hd = fma(Hs[k * K + j], d[j], hd);
+                const float dn = (float)(d[k] * B[k] / fmax(hd, 1e-30));
+                if (!isfinite(dn)) bad |= ST_NUMERIC;
+                D[(int64_t)k * Nk + l] = dn;
+                dsm[k][lane] = (double)dn;
+                bd += B[k] * (double)dn;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) dsm[k][lane] = 0.0;
         }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            double hd = 0.0;
-#pragma unroll
-            for (int j = 0; j < K; ++j) hd = fma(Hs[k * K + j], d[j], hd);
-            const float dn = (float)(d[k] * B[k] / fmax(hd, 1e-30));
-            if (!isfinite(dn)) bad |= ST_NUMERIC;
-            D[(int64_t)k * Nk + l] = dn;
-            dsm[k][tid] = (double)dn;
-            bd += B[k] * (double)dn;
+        bd = warp_sum(bd);
+        bad = warp_or(bad);
+        if (lane == 0) {
+            dpart[bx] = bd;
+            if (bad) atomicOr(status, bad);
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < K; ++k) dsm[k][tid] = 0.0;
-    }
-    bd = warp_sum(bd);
-    bad = warp_or(bad);
-    if (lane == 0) {
-        red[warp] = bd;
-        if (bad) atomicOr(status, bad);
     }
     __syncthreads();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < DT / 32; ++w) s += red[w];
-        dpart[blockIdx.x] = s;
-    }
-    // per-block partial of G_new = D_new D_new^T (fixed order over this block's lambdas)
-    for (int t = tid; t < K * K; t += DT) {
+    for (int t = tid; t < KK; t += 256) {
         const int a = t / K, b = t - (t / K) * K;
         double s = 0.0;
-        for (int u = 0; u < DT; ++u) s = fma(dsm[a][u], dsm[b][u], s);
-        Gpart[(int64_t)blockIdx.x * K * K + t] = s;
+        for (int u = 0; u < 32; ++u) s = fma(dsm[a][u], dsm[b][u], s);
+        Gpart[(int64_t)bx * KK + t] = s;
     }
+    if (tid == 0) colcnt[bx] = 0u;
     __threadfence();
     __syncthreads();
-    if (tid == 0) is_last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    if (tid == 0) flag = (atomicAdd(counter, 1u) == (unsigned)nbx - 1);
     __syncthreads();
-    if (!is_last) return;
+    if (!flag) return;
     __threadfence();
-    // ---- last block: objective terms and G for the next row pass
-    __shared__ double sc[4];
+    // ---- global finalize: objective terms and G for the next row pass
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int i = tid; i < nblk_v; i += 256) {
+        v0 += __ldcg(vpart + 2 * i);
+        v1 += __ldcg(vpart + 2 * i + 1);
+    }
+    if (first)
+        for (int i = tid; i < nby; i += 256) v1 += __ldcg(ypart + i);
+    for (int i = tid; i < nbx; i += 256) v2 += __ldcg(dpart + i);
+    const double va = block_sum(v0, red);
+    const double ysq_new = block_sum(v1, red);
+    const double bdot = block_sum(v2, red);
     if (tid == 0) {
         double ysq;
         if (first) {
-            ysq = 0.0;
-            for (int i = 0; i < nblk_v; ++i) ysq += __ldcg(vpart + 2 * i + 1);
+            ysq = ysq_new;
             *ysq_store = ysq;
             if (!(ysq > 0.0)) atomicOr(status, (unsigned)ST_Y_ALLZERO);
         } else {
             ysq = *ysq_store;
         }
-        double va = 0.0, bdot = 0.0;
-        for (int i = 0; i < nblk_v; ++i) va += __ldcg(vpart + 2 * i);
-        for (int i = 0; i < (int)gridDim.x; ++i) bdot += __ldcg(dpart + i);
         double hg_old = 0.0;
-        for (int t = 0; t < K * K; ++t) hg_old += Hs[t] * Gd[t];
+        for (int t = 0; t < KK; ++t) hg_old += Hs[t] * Gd[t];
         sc[0] = ysq;
         sc[1] = va;
         sc[2] = bdot;
         sc[3] = hg_old;
     }
     __syncthreads();
-    for (int t = tid; t < K * K; t += DT) {
+    for (int t = tid; t < KK * NS; t += 256) {
+        const int o = t % KK, sub = t / KK;
         double s = 0.0;
-        for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(Gpart + (int64_t)i * K * K + t);
-        Gd[t] = s;
+        for (int i = sub; i < nbx; i += NS) s += __ldcg(Gpart + (int64_t)i * KK + o);
+        hs[sub][o] = s;
+    }
+    __syncthreads();
+    for (int o = tid; o < KK; o += 256) {
+        double s = 0.0;
+        for (int sub = 0; sub < NS; ++sub) s += hs[sub][o];
+        Gd[o] = s;
     }
     __syncthreads();
     if (tid == 0) {
         double hg_new = 0.0;
-        for (int t = 0; t < K * K; ++t) hg_new += Hs[t] * Gd[t];
+        for (int t = 0; t < KK; ++t) hg_new += Hs[t] * Gd[t];
         if (obj2) {
             obj2[0] = sc[0] - 2.0 * sc[1] + sc[3];
             obj2[1] = sc[0] - 2.0 * sc[2] + hg_new;
@@ -412,6 +509,7 @@ __global__ void __launch_bounds__(DT) k_dupdate(const float* __restrict__ Bpart,
     M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+int64_t Np_(const Geometry& g) { return (int64_t)g.Nv * g.Nr * g.Nc; }
 
 }  // namespace
 
@@ -419,35 +517,44 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     NmfPlan p{};
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     p.Nkp = (g.Nk + 3) & ~3;
+    p.nbx = (g.Nk + 31) / 32;
+    p.fused = nmf_fused_plan(g, num_sms, &p);
+    // two-pass fallback (K > 8 or very long spectra)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
-    // row pass: 256-thread blocks, up to `occ` per SM (smem-limited), static schedule
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
     const int64_t groups = (Np + VW * RPW - 1) / (VW * RPW);
     p.nblk_v = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)num_sms * occ));
-    // column pass: one lambda quad per thread
     const int nq = p.Nkp / 4;
     p.nlam_blk = (nq + BT_MAX - 1) / BT_MAX;
     const int per = (nq + p.nlam_blk - 1) / p.nlam_blk;
     p.bthreads = std::max(32, ((per + 31) / 32) * 32);
-    const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 8) / p.nlam_blk);
+    const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 2) / p.nlam_blk);
     p.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(want, (Np + BROWS - 1) / BROWS));
     p.rows_per_chunk = (Np + p.nchunk - 1) / p.nchunk;
     p.nchunk = (int)((Np + p.rows_per_chunk - 1) / p.rows_per_chunk);
     if (p.nchunk < 1) p.nchunk = 1;
-    p.nblk_d = (g.Nk + DT - 1) / DT;
+    p.P = p.fused ? p.PB : p.nchunk;
+    p.PH = p.fused ? p.nblk_f : p.nchunk;
+    p.nvp = p.fused ? p.nblk_f : p.nblk_v;
     return p;
 }
 
 size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     const size_t KK = (size_t)g.K * g.K;
     size_t b = 0;
-    b += align256(KK * sizeof(double));                          // Gd
-    b += align256((size_t)p.nblk_v * 2 * sizeof(double));        // vpart
-    b += align256((size_t)p.nblk_d * sizeof(double));            // dpart
-    b += align256((size_t)p.nblk_d * KK * sizeof(double));       // Gpart
-    b += align256(sizeof(double));                               // ysq
-    b += align256((size_t)p.nchunk * KK * sizeof(double));       // Hpart
-    b += align256((size_t)p.nchunk * g.K * p.Nkp * sizeof(float));  // Bpart
+    b += align256(KK * sizeof(double));                               // Gd
+    b += align256((size_t)p.nvp * 2 * sizeof(double));                // vpart
+    b += align256((size_t)p.nbx * sizeof(double));                    // dpart
+    b += align256((size_t)p.nbx * KK * sizeof(double));               // Gpart
+    b += align256(sizeof(double));                                    // ysq
+    b += align256((size_t)p.PH * KK * sizeof(double));                // Hpart
+    b += align256((size_t)p.P * g.K * p.Nkp * sizeof(float));         // Bpart
+    b += align256((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));   // L2B
+    b += align256((size_t)p.nbx * DG2 * KK * sizeof(double));         // L2H
+    if (p.fused) {
+        b += align256((size_t)Np_(g) * p.Nkp * sizeof(float));        // Yp
+        b += align256((size_t)p.nby * sizeof(double));                // ypart
+    }
     return b;
 }
 
@@ -461,18 +568,29 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
         return r;
     };
     w.Gd = (double*)take(KK * sizeof(double));
-    w.vpart = (double*)take((size_t)p.nblk_v * 2 * sizeof(double));
-    w.dpart = (double*)take((size_t)p.nblk_d * sizeof(double));
-    w.Gpart = (double*)take((size_t)p.nblk_d * KK * sizeof(double));
+    w.vpart = (double*)take((size_t)p.nvp * 2 * sizeof(double));
+    w.dpart = (double*)take((size_t)p.nbx * sizeof(double));
+    w.Gpart = (double*)take((size_t)p.nbx * KK * sizeof(double));
     w.ysq = (double*)take(sizeof(double));
-    w.Hpart = (double*)take((size_t)p.nchunk * KK * sizeof(double));
-    w.Bpart = (float*)take((size_t)p.nchunk * g.K * p.Nkp * sizeof(float));
+    w.Hpart = (double*)take((size_t)p.PH * KK * sizeof(double));
+    w.Bpart = (float*)take((size_t)p.P * g.K * p.Nkp * sizeof(float));
+    w.L2B = (double*)take((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));
+    w.L2H = (double*)take((size_t)p.nbx * DG2 * KK * sizeof(double));
+    if (p.fused) {
+        w.Yp = (float*)take((size_t)Np_(g) * p.Nkp * sizeof(float));
+        w.ypart = (double*)take((size_t)p.nby * sizeof(double));
+    }
     return w;
 }
 
-cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* D,
-                            unsigned* status, cudaStream_t s) {
-    (void)p;
+int nmf_init_launches(const NmfPlan& p) { return p.fused ? 2 : 1; }
+
+cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                            const float* D, unsigned* status, cudaStream_t s) {
+    if (p.fused) {
+        cudaError_t e = nmf_yplus_launch(g, p, w, Y, ld_y, status, s);
+        if (e != cudaSuccess) return e;
+    }
     switch (g.K) {
 #define M(KV)                                                               \
     case KV:                                                                \
@@ -491,23 +609,32 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
                           int64_t ld, float* V, float* D, bool first, double* obj2,
                           unsigned* status, unsigned* counter, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    static bool attr_done = false;  // per-K instantiation
-    if (!attr_done) {
-        cudaFuncSetAttribute(k_vstep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        cudaFuncSetAttribute(k_vstep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-        attr_done = true;
+    if (p.fused) {
+        cudaError_t e = nmf_fused_launch(g, p, w, V, D, status, s);
+        if (e != cudaSuccess) return e;
+    } else {
+        static bool attr_done = false;  // per-K instantiation
+        if (!attr_done) {
+            cudaFuncSetAttribute(k_vstep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            cudaFuncSetAttribute(k_vstep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            attr_done = true;
+        }
+        if (first)
+            k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
+        else
+            k_vstep<K, false><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
+        dim3 gb(p.nchunk, p.nlam_blk);
+        k_bpart<K><<<gb, p.bthreads, 0, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, p.rows_per_chunk, w.Bpart, w.Hpart);
     }
-    if (first)
-        k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
-    else
-        k_vstep<K, false><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
-    dim3 gb(p.nchunk, p.nlam_blk);
-    k_bpart<K><<<gb, p.bthreads, 0, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, p.rows_per_chunk, w.Bpart, w.Hpart);
-    k_dupdate<K><<<p.nblk_d, DT, 0, s>>>(w.Bpart, w.Hpart, p.nchunk, g.Nk, p.Nkp, D, w.Gd, w.vpart,
-                                         p.nblk_v, w.dpart, w.Gpart, w.ysq, first ? 1 : 0,
-                                         obj2, counter, status);
+    dim3 gd(p.nbx, DG2);
+    k_dred<K><<<gd, 256, 0, s>>>(w.Bpart, w.Hpart, p.P, p.PH, g.Nk, p.Nkp, D, w.Gd, w.vpart, p.nvp,
+                                 w.ypart, p.fused ? p.nby : 0, w.L2B,
+                                 w.L2H, w.dpart, w.Gpart, w.ysq, first ? 1 : 0, obj2, counter + 1,
+                                 counter, status);
     return cudaGetLastError();
 }
+
+int nmf_launches_per_iter(const NmfPlan& p) { return p.fused ? 2 : 3; }
 
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
                             int64_t ld_y, float* V, float* D, bool first, double* obj2,
