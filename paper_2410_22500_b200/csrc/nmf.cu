@@ -534,8 +534,8 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.nchunk = (int)((Np + p.rows_per_chunk - 1) / p.rows_per_chunk);
     if (p.nchunk < 1) p.nchunk = 1;
     p.P = p.fused ? p.PB : p.nchunk;
-    p.PH = p.fused ? p.nblk_f : p.nchunk;
-    p.nvp = p.fused ? p.nblk_f : p.nblk_v;
+    p.PH = p.fused ? p.PB : p.nchunk;
+    p.nvp = p.fused ? p.PB : p.nblk_v;
     return p;
 }
 

@@ -27,13 +27,12 @@
 namespace hsnct {
 namespace {
 
-constexpr int R = 8;               // rows per tile
-constexpr int RG = 4;              // rows per compute group
-constexpr int NG = R / RG;         // compute groups
+constexpr int RG = 4;              // rows per tile (= rows per compute-group step)
+constexpr int NG = 2;              // compute groups (alternate tiles)
 constexpr int GW = 4;              // warps per group
 constexpr int CW = NG * GW;        // compute warps
 constexpr int TG = GW * 32;        // threads per group
-constexpr int NTHREADS = (CW + 1) * 32;
+constexpr int NTHREADS = (CW + NG) * 32;   // + one reducer/producer warp per group
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -172,41 +171,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
                                                            double* __restrict__ Hpart,
                                                            double* __restrict__ vpart,
                                                            unsigned* __restrict__ status) {
-    constexpr int RK = R * K;
+    // Tiles are RG rows; the CTA's tile sequence j = 0, 1, 2, ... alternates between
+    // the two compute groups (group j % 2).  A group runs phase 1, waits for the
+    // reducer's V update of that tile, runs phase 2 and releases the buffer, while
+    // the other group computes its own tile; the ring keeps NBUF - 2 tiles in flight.
     constexpr int GK = RG * K;
     constexpr int KP = (K + 3) & ~3;
     constexpr int DS = 2 * TG * LP;  // smem row stride of D (>= Nkp, zero padded)
     constexpr int KK = K * K;
     extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF], partb[2], vnb[2];
-    __shared__ float red[2][CW][GK];
-    __shared__ __align__(16) float Vn[2][R][KP];
-    __shared__ float Vo[R][K];
+    __shared__ __align__(8) uint64_t full[NBUF], empty[NBUF], partb[NG], vnb[NG];
+    __shared__ float red[NG][GW][GK];
+    __shared__ __align__(16) float Vn[NG][RG][KP];
     __shared__ float Gs[KK];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntiles = (Np + R - 1) / R;
+    const int64_t ntiles = (Np + RG - 1) / RG;
     const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const size_t tile_floats = (size_t)R * Nkp;
-    float* ring = smem;                                  // [NBUF][R][Nkp] + slack DS
+    const size_t tile_floats = (size_t)RG * Nkp + RG * K;   // Y+ rows, then the old V rows
+    float* ring = smem;                                  // [NBUF][RG*Nkp + RG*K] + slack DS
     float* Ds = smem + NBUF * tile_floats + DS;          // [K][DS]
 
-    // zero the ring (+ slack read past the last row) and stage D (zero padded)
     for (size_t i = tid; i < NBUF * tile_floats + DS; i += NTHREADS) ring[i] = 0.f;
     for (int i = tid; i < K * DS; i += NTHREADS) {
         const int k = i / DS, l = i - k * DS;
         Ds[i] = (l < Nk) ? D[(int64_t)k * Nk + l] : 0.f;
     }
     for (int i = tid; i < KK; i += NTHREADS) Gs[i] = (float)Gd[i];
-    for (int i = tid; i < 2 * R * KP; i += NTHREADS) (&Vn[0][0][0])[i] = 0.f;
+    for (int i = tid; i < NG * RG * KP; i += NTHREADS) (&Vn[0][0][0])[i] = 0.f;
     if (tid == 0) {
         for (int b = 0; b < NBUF; ++b) {
             mbar_init(&full[b], 1);
-            mbar_init(&empty[b], CW * 32);
+            mbar_init(&empty[b], TG);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&partb[b], CW * 32);
-            mbar_init(&vnb[b], 32);
+        for (int g = 0; g < NG; ++g) {
+            mbar_init(&partb[g], TG);
+            mbar_init(&vnb[g], 32);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
     if (warp < CW) {
         // ======================= compute warps =======================
         const int g = warp / GW;
+        const int wg = warp - g * GW;
         const int t = tid - g * TG;
         float2 bacc[K][LP];
 #pragma unroll
@@ -222,18 +223,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
 #pragma unroll
             for (int i = 0; i < LP; ++i) bacc[k][i] = make_float2(0.f, 0.f);
         const float* dbase = Ds + 2 * t;
-
-        auto phase2 = [&](int64_t jj) {
-            const int b = (int)(jj % NBUF);
-            const int s = (int)(jj & 1);
-            mbar_wait(&vnb[s], (unsigned)((jj >> 1) & 1));
-            const float* yb = ring + (size_t)b * tile_floats + (size_t)(g * RG) * Nkp + 2 * t;
+        int64_t kth = 0;  // this group's tile count
+        for (int64_t j = g; j < nmine; j += NG, ++kth) {
+            const int b = (int)(j % NBUF);
+            mbar_wait(&full[b], (unsigned)((j / NBUF) & 1));
+            const float* yb = ring + (size_t)b * tile_floats + 2 * t;
+            // ---- phase 1
+            float part[GK];
+#pragma unroll
+            for (int x = 0; x < GK; ++x) part[x] = 0.f;
+#pragma unroll
+            for (int i = 0; i < LP; ++i) {
+                float2 y[RG];
+#pragma unroll
+                for (int r = 0; r < RG; ++r)
+                    y[r] = *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const float2 d = *reinterpret_cast<const float2*>(dbase + k * DS + 2 * TG * i);
+#pragma unroll
+                    for (int r = 0; r < RG; ++r)
+                        part[r * K + k] = fmaf(y[r].x, d.x, fmaf(y[r].y, d.y, part[r * K + k]));
+                }
+            }
+            tr_step<16, GK>(part, lane);
+            if (((unsigned)lane & tr_bfly(GK)) == 0) {
+                const int base = tr_base<GK>(lane);
+#pragma unroll
+                for (int x = 0; x < tr_nout(GK); ++x) red[g][wg][base + x] = part[x];
+            }
+            mbar_arrive(&partb[g]);
+            // ---- phase 2 (after the reducer's V update of this tile)
+            mbar_wait(&vnb[g], (unsigned)(kth & 1));
             float vr[RG][KP];
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
 #pragma unroll
                 for (int q = 0; q < KP / 4; ++q) {
-                    const float4 v4 = reinterpret_cast<const float4*>(&Vn[s][g * RG + r][0])[q];
+                    const float4 v4 = reinterpret_cast<const float4*>(&Vn[g][r][0])[q];
                     vr[r][4 * q + 0] = v4.x;
                     vr[r][4 * q + 1] = v4.y;
                     vr[r][4 * q + 2] = v4.z;
@@ -258,39 +285,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
                 }
             }
             mbar_arrive(&empty[b]);
-        };
-
-        for (int64_t j = 0; j < nmine; ++j) {
-            const int b = (int)(j % NBUF);
-            mbar_wait(&full[b], (unsigned)((j / NBUF) & 1));
-            const float* yb = ring + (size_t)b * tile_floats + (size_t)(g * RG) * Nkp + 2 * t;
-            float part[GK];
-#pragma unroll
-            for (int x = 0; x < GK; ++x) part[x] = 0.f;
-#pragma unroll
-            for (int i = 0; i < LP; ++i) {
-                float2 y[RG];
-#pragma unroll
-                for (int r = 0; r < RG; ++r)
-                    y[r] = *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i);
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float2 d = *reinterpret_cast<const float2*>(dbase + k * DS + 2 * TG * i);
-#pragma unroll
-                    for (int r = 0; r < RG; ++r)
-                        part[r * K + k] = fmaf(y[r].x, d.x, fmaf(y[r].y, d.y, part[r * K + k]));
-                }
-            }
-            tr_step<16, GK>(part, lane);
-            if (((unsigned)lane & tr_bfly(GK)) == 0) {
-                const int base = tr_base<GK>(lane);
-#pragma unroll
-                for (int x = 0; x < tr_nout(GK); ++x) red[j & 1][warp][base + x] = part[x];
-            }
-            mbar_arrive(&partb[j & 1]);
-            if (j > 0) phase2(j - 1);
         }
-        if (nmine > 0) phase2(nmine - 1);
         // CTA partial of B for this group
 #pragma unroll
         for (int i = 0; i < LP; ++i) {
@@ -303,69 +298,81 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
             }
         }
     } else {
-        // ======================= reducer / producer warp =======================
+        // =============== reducer / producer warp of group g (tiles j = g mod NG) ===============
+        const int g = warp - CW;
         auto issue = [&](int64_t jj) {
             const int b = (int)(jj % NBUF);
-            const int64_t r0 = (blockIdx.x + jj * gridDim.x) * R;
-            const int nv = (int)min((int64_t)R, Np - r0);
+            const int64_t r0 = (blockIdx.x + jj * gridDim.x) * RG;
+            const int nv = (int)min((int64_t)RG, Np - r0);
             const unsigned bytes = (unsigned)(nv * Nkp * sizeof(float));
-            mbar_expect_tx(&full[b], bytes);
-            bulk_g2s(ring + (size_t)b * tile_floats, Yp + r0 * Nkp, bytes, &full[b]);
+            const unsigned vbytes = nv == RG ? (unsigned)(RG * K * sizeof(float)) : 0u;  // 16K bytes
+            mbar_expect_tx(&full[b], bytes + vbytes);
+            float* slot = ring + (size_t)b * tile_floats;
+            bulk_g2s(slot, Yp + r0 * Nkp, bytes, &full[b]);
+            if (vbytes) bulk_g2s(slot + (size_t)RG * Nkp, V + r0 * K, vbytes, &full[b]);
         };
         if (lane == 0) {
             fence_proxy_async();
-            for (int64_t jj = 0; jj < min((int64_t)NBUF, nmine); ++jj) issue(jj);
+            for (int64_t jj = g; jj < min((int64_t)NBUF, nmine); jj += NG) issue(jj);
         }
         double vdotA = 0.0;
         double hacc[(KK + 31) / 32];
 #pragma unroll
         for (int x = 0; x < (KK + 31) / 32; ++x) hacc[x] = 0.0;
         unsigned bad = 0;
-        // old V rows of the first tile
-        if (nmine > 0) {
-            const int64_t r0 = (int64_t)blockIdx.x * R;
-            for (int s = lane; s < RK; s += 32) {
-                const int r = s / K;
-                Vo[r][s - r * K] = (r0 + r < Np) ? V[r0 * K + s] : 0.f;
-            }
-        }
-        __syncwarp();
-        for (int64_t j = 0; j < nmine; ++j) {
-            const int64_t r0 = (blockIdx.x + j * gridDim.x) * R;
-            const int nv = (int)min((int64_t)R, Np - r0);
-            const int sb = (int)(j & 1);
-            mbar_wait(&partb[sb], (unsigned)((j >> 1) & 1));
-            float vnew[(RK + 31) / 32];
+        int64_t kth = 0;
+        for (int64_t j = g; j < nmine; j += NG, ++kth) {
+            const int64_t r0 = (blockIdx.x + j * gridDim.x) * RG;
+            const int nv = (int)min((int64_t)RG, Np - r0);
+            const int b = (int)(j % NBUF);
+            mbar_wait(&full[b], (unsigned)((j / NBUF) & 1));
+            const float* vslot = ring + (size_t)b * tile_floats + (size_t)RG * Nkp;
+            float vo_all[(GK + 31) / 32][K];
+            float vo_me[(GK + 31) / 32];
 #pragma unroll
-            for (int u = 0; u < (RK + 31) / 32; ++u) {
+            for (int u = 0; u < (GK + 31) / 32; ++u) {
+                const int s = lane + 32 * u;
+                const int r = (s < GK ? s : 0) / K;
+#pragma unroll
+                for (int jj = 0; jj < K; ++jj)
+                    vo_all[u][jj] = nv == RG ? vslot[r * K + jj] : ((r < nv) ? V[(r0 + r) * K + jj] : 0.f);
+                vo_me[u] = vo_all[u][s < GK ? s - r * K : 0];
+            }
+            mbar_wait(&partb[g], (unsigned)(kth & 1));
+            float vnew[(GK + 31) / 32], aval[(GK + 31) / 32];
+#pragma unroll
+            for (int u = 0; u < (GK + 31) / 32; ++u) {
                 const int s = lane + 32 * u;
                 vnew[u] = 0.f;
-                if (s < RK) {
+                aval[u] = 0.f;
+                if (s < GK) {
                     const int r = s / K, k = s - (s / K) * K;
-                    const int gg = r / RG, idx = (r - gg * RG) * K + k;
                     float a = 0.f;
 #pragma unroll
-                    for (int w = 0; w < GW; ++w) a += red[sb][gg * GW + w][idx];
+                    for (int w = 0; w < GW; ++w) a += red[g][w][s];
                     float vg = 0.f;
 #pragma unroll
-                    for (int jj = 0; jj < K; ++jj) vg = fmaf(Vo[r][jj], Gs[jj * K + k], vg);
-                    const float vo = Vo[r][k];
-                    if (j == 0 && r < nv && !(isfinite(vo) && vo >= 0.f)) bad |= ST_INIT_BAD;
-                    float vn = __fdiv_rn(vo * a, fmaxf(vg, 1e-30f));
+                    for (int jj = 0; jj < K; ++jj) vg = fmaf(vo_all[u][jj], Gs[jj * K + k], vg);
+                    float vn = __fdiv_rn(vo_me[u] * a, fmaxf(vg, 1e-30f));
                     if (r >= nv) vn = 0.f;
-                    if (!isfinite(vn)) bad |= ST_NUMERIC;
-                    if (r < nv) V[r0 * K + s] = vn;
-                    vdotA += (double)vn * (double)a;
                     vnew[u] = vn;
+                    aval[u] = a;
+                    Vn[g][r][k] = vn;
                 }
             }
-#pragma unroll
-            for (int u = 0; u < (RK + 31) / 32; ++u) {
-                const int s = lane + 32 * u;
-                if (s < RK) Vn[sb][s / K][s - (s / K) * K] = vnew[u];
-            }
             __syncwarp();
-            // H += V_new^T V_new over the tile (fp64, fixed order)
+            mbar_arrive(&vnb[g]);
+            // off the compute warps' critical path: V store, checks, objective, H, refill
+#pragma unroll
+            for (int u = 0; u < (GK + 31) / 32; ++u) {
+                const int s = lane + 32 * u;
+                if (s < GK && s / K < nv) {
+                    if (j < NG && !(isfinite(vo_me[u]) && vo_me[u] >= 0.f)) bad |= ST_INIT_BAD;
+                    if (!isfinite(vnew[u])) bad |= ST_NUMERIC;
+                    V[r0 * K + s] = vnew[u];
+                    vdotA += (double)vnew[u] * (double)aval[u];
+                }
+            }
 #pragma unroll
             for (int x = 0; x < (KK + 31) / 32; ++x) {
                 const int tt = lane + 32 * x;
@@ -373,23 +380,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
                     const int a = tt / K, c = tt - (tt / K) * K;
                     double s = 0.0;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) s = fma((double)Vn[sb][r][a], (double)Vn[sb][r][c], s);
+                    for (int r = 0; r < RG; ++r) s = fma((double)Vn[g][r][a], (double)Vn[g][r][c], s);
                     hacc[x] += s;
                 }
             }
-            mbar_arrive(&vnb[sb]);
-            // old V rows of the next tile
-            if (j + 1 < nmine) {
-                const int64_t r1 = (blockIdx.x + (j + 1) * gridDim.x) * R;
-                for (int s = lane; s < RK; s += 32) {
-                    const int r = s / K;
-                    Vo[r][s - r * K] = (r1 + r < Np) ? V[r1 * K + s] : 0.f;
-                }
-            }
-            __syncwarp();
-            // refill the ring: tile j-1+NBUF goes into the buffer phase 2 of tile j-1 frees
-            if (j >= 1 && j - 1 + NBUF < nmine) {
-                const int64_t m = j - 1;
+            // refill: this group's previous tile (j - NG) was released before part(j)
+            if (j >= NG && j - NG + NBUF < nmine) {
+                const int64_t m = j - NG;
                 mbar_wait(&empty[m % NBUF], (unsigned)((m / NBUF) & 1));
                 if (lane == 0) {
                     fence_proxy_async();
@@ -401,14 +398,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
 #pragma unroll
         for (int o = 16; o; o >>= 1) bad |= __shfl_xor_sync(0xffffffffu, bad, o);
         if (lane == 0) {
-            vpart[2 * blockIdx.x] = vdotA;
-            vpart[2 * blockIdx.x + 1] = 0.0;
+            vpart[2 * ((int64_t)blockIdx.x * NG + g)] = vdotA;
+            vpart[2 * ((int64_t)blockIdx.x * NG + g) + 1] = 0.0;
             if (bad) atomicOr(status, bad);
         }
 #pragma unroll
         for (int x = 0; x < (KK + 31) / 32; ++x) {
             const int tt = lane + 32 * x;
-            if (tt < KK) Hpart[(int64_t)blockIdx.x * KK + tt] = hacc[x];
+            if (tt < KK) Hpart[((int64_t)blockIdx.x * NG + g) * KK + tt] = hacc[x];
         }
     }
 }
@@ -422,10 +419,10 @@ constexpr int lp_cap(int K) {
 }
 
 static int nbuf_for(int Nkp, int LP, int K) {
-    const size_t tile = (size_t)R * Nkp * sizeof(float);
+    const size_t tile = ((size_t)RG * Nkp + RG * K) * sizeof(float);
     const size_t fixed = (size_t)(2 * TG * LP) * sizeof(float) * (1 + K);
-    for (int nb = 4; nb >= 2; --nb)
-        if (nb * tile + fixed <= 200 * 1024) return nb;
+    for (int nb = 8; nb >= 4; nb -= 2)   // even: reducer g refills only group-g tiles
+        if (nb * tile + fixed <= 205 * 1024) return nb;
     return 0;
 }
 
@@ -436,13 +433,13 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int LP = (pairs + TG - 1) / TG;
     if (LP > lp_cap(g.K)) return false;
     const int nbuf = nbuf_for(Nkp, LP, g.K);
-    if (nbuf < 2) return false;
+    if (nbuf < 4) return false;
     p->LP = LP;
     p->nbuf = nbuf;
     p->fthreads = NTHREADS;
-    p->smem_f = ((size_t)nbuf * R * Nkp + (size_t)2 * TG * LP * (1 + g.K)) * sizeof(float);
+    p->smem_f = ((size_t)nbuf * (RG * Nkp + RG * g.K) + (size_t)2 * TG * LP * (1 + g.K)) * sizeof(float);
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    const int64_t ntiles = (Np + R - 1) / R;
+    const int64_t ntiles = (Np + RG - 1) / RG;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));
     p->PB = p->nblk_f * NG;
     p->nby = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (Np * (Nkp / 4) + 255) / 256));
@@ -467,9 +464,9 @@ template <int K, int LP>
 static cudaError_t fused_kl(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
                             unsigned* status, cudaStream_t s) {
     switch (p.nbuf) {
-        case 2: return fused_klb<K, LP, 2>(g, p, w, V, D, status, s);
-        case 3: return fused_klb<K, LP, 3>(g, p, w, V, D, status, s);
         case 4: return fused_klb<K, LP, 4>(g, p, w, V, D, status, s);
+        case 6: return fused_klb<K, LP, 6>(g, p, w, V, D, status, s);
+        case 8: return fused_klb<K, LP, 8>(g, p, w, V, D, status, s);
         default: return cudaErrorInvalidValue;
     }
 }
