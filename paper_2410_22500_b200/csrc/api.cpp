@@ -141,6 +141,17 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
     const NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
+    if (h->nmf.persist) {
+        const int nbx = (h->g.Nk + 31) / 32;
+        cudaError_t e = nmf_persist_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1,
+                                           h->t.status, s);
+        if (e == cudaSuccess) {
+            h->launches += 1;
+            return HSNCT_OK;
+        }
+        // cooperative launch refused (e.g. SMs shared with other work): per-iteration launches
+        (void)cudaGetLastError();
+    }
     for (int it = 0; it < n_iter; ++it) {
         CK(nmf_launch_iter(h->g, h->nmf, w, Y, ld, V, D, it == 0, obj ? obj + 2 * it : nullptr,
                            h->t.status, h->t.counter, s),
@@ -284,7 +295,7 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     al((void**)&h->t.Hhat, g.P * sizeof(float));
     al((void**)&h->t.twiddle, (g.P / 2) * sizeof(float2));
     al((void**)&h->t.status, sizeof(unsigned));
-    al((void**)&h->t.counter, (size_t)(2 + (g.Nk + 31) / 32) * sizeof(unsigned));
+    al((void**)&h->t.counter, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->status_host, sizeof(unsigned), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaMemcpy(h->t.cos_t, cs.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->t.sin_t, sn.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
@@ -292,7 +303,7 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     if (e == cudaSuccess)
         e = cudaMemcpy(h->t.twiddle, tw.data(), (g.P / 2) * sizeof(float2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(h->t.status, 0, sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, (size_t)(2 + (g.Nk + 31) / 32) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         hsnct_destroy(h);

@@ -44,6 +44,7 @@ struct NmfPlan {
     int nvp;         // number of per-CTA objective partials
     // fused single-pass path (nmf_fused.cu), K <= 8
     bool fused;
+    bool persist;    // run all iterations in one cooperative launch (fused path)
     int LP;          // lambda pairs per thread
     int nbuf;        // tile ring depth
     int PB;          // B partials of the fused kernel (2 per CTA)
@@ -83,7 +84,10 @@ cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w,
                             int64_t ld_y, float* V, float* D, bool first, double* obj2,
                             unsigned* status, unsigned* counter, cudaStream_t s);
 cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
-                             unsigned* status, cudaStream_t s);
+                             bool first, unsigned* status, cudaStream_t s);
+// All n_iter iterations in one cooperative launch (fused path); bar = 2 zeroed words.
+cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
+                               double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                              unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);

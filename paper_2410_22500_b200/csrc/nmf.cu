@@ -11,6 +11,7 @@
 // Everything is deterministic: static schedules, fixed-order reductions, no
 // floating-point atomics (the only atomics are integer status / ticket words).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -519,6 +520,8 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.Nkp = (g.Nk + 3) & ~3;
     p.nbx = (g.Nk + 31) / 32;
     p.fused = nmf_fused_plan(g, num_sms, &p);
+    const char* np_env = getenv("HSNCT_NO_PERSIST");
+    p.persist = p.fused && !(np_env && np_env[0] == '1');
     // two-pass fallback (K > 8 or very long spectra)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
@@ -544,8 +547,8 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     size_t b = 0;
     b += align256(KK * sizeof(double));                               // Gd
     b += align256((size_t)p.nvp * 2 * sizeof(double));                // vpart
-    b += align256((size_t)p.nbx * sizeof(double));                    // dpart
-    b += align256((size_t)p.nbx * KK * sizeof(double));               // Gpart
+    b += align256((size_t)std::max(p.nbx, p.nblk_f) * sizeof(double));        // dpart
+    b += align256((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));   // Gpart
     b += align256(sizeof(double));                                    // ysq
     b += align256((size_t)p.PH * KK * sizeof(double));                // Hpart
     b += align256((size_t)p.P * g.K * p.Nkp * sizeof(float));         // Bpart
@@ -569,8 +572,8 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
     };
     w.Gd = (double*)take(KK * sizeof(double));
     w.vpart = (double*)take((size_t)p.nvp * 2 * sizeof(double));
-    w.dpart = (double*)take((size_t)p.nbx * sizeof(double));
-    w.Gpart = (double*)take((size_t)p.nbx * KK * sizeof(double));
+    w.dpart = (double*)take((size_t)std::max(p.nbx, p.nblk_f) * sizeof(double));
+    w.Gpart = (double*)take((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));
     w.ysq = (double*)take(sizeof(double));
     w.Hpart = (double*)take((size_t)p.PH * KK * sizeof(double));
     w.Bpart = (float*)take((size_t)p.P * g.K * p.Nkp * sizeof(float));
@@ -610,7 +613,7 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
                           unsigned* status, unsigned* counter, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     if (p.fused) {
-        cudaError_t e = nmf_fused_launch(g, p, w, V, D, status, s);
+        cudaError_t e = nmf_fused_launch(g, p, w, V, D, first, status, s);
         if (e != cudaSuccess) return e;
     } else {
         static bool attr_done = false;  // per-K instantiation
