@@ -271,7 +271,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"C{cfg.idx}", {}).get("nmf_iter_dram_bytes")
-    roof = {"bound": "hbm", "kernel": "NMF iteration (k_vstep + k_bpart + k_dupdate)",
+    roof = {"bound": "hbm", "kernel": "subspace_decompose (k_nmf_persist: all iterations in one cooperative launch; k_yplus + k_gram_init once per call)",
             "achieved": nmf_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": nmf_gbs / peaks["hbm_gbs"], "traffic": traffic,
             "algorithmic_bytes_per_unit": nmf_bytes_iter, "unit_of_work": "one NMF iteration",

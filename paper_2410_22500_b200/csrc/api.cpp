@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -26,6 +27,8 @@ struct hsnct_s {
     NmfPlan nmf{};
     unsigned* status_host = nullptr;  // pinned mirror of t.status
     uint64_t launches = 0;
+    uint64_t* trace = nullptr;        // diagnostics buffer (HSNCT_TRACE=1 at create)
+    int trace_iters = 0;
 };
 
 namespace {
@@ -138,7 +141,9 @@ hsnct_status check_y(const Geometry& g, const float* Y, int64_t ld, const char* 
 hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, float* D, int n_iter,
                            double* obj, void* ws, cudaStream_t s) {
     if (n_iter == 0) return HSNCT_OK;
-    const NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
+    NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
+    w.trace = h->trace;
+    w.trace_iters = h->trace_iters;
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
     if (h->nmf.persist) {
@@ -153,7 +158,7 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
         (void)cudaGetLastError();
     }
     for (int it = 0; it < n_iter; ++it) {
-        CK(nmf_launch_iter(h->g, h->nmf, w, Y, ld, V, D, it == 0, obj ? obj + 2 * it : nullptr,
+        CK(nmf_launch_iter(h->g, h->nmf, w, Y, ld, V, D, it, obj ? obj + 2 * it : nullptr,
                            h->t.status, h->t.counter, s),
            "decompose iteration");
         h->launches += nmf_launches_per_iter(h->nmf);
@@ -304,6 +309,13 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
         e = cudaMemcpy(h->t.twiddle, tw.data(), (g.P / 2) * sizeof(float2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(h->t.status, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
+    const char* tr = getenv("HSNCT_TRACE");
+    if (e == cudaSuccess && tr && tr[0] == '1' && h->nmf.persist) {
+        h->trace_iters = 256;
+        const size_t tb = (size_t)h->trace_iters * h->nmf.nblk_f * TRACE_SLOTS * sizeof(uint64_t);
+        e = cudaMalloc((void**)&h->trace, tb);
+        if (e == cudaSuccess) e = cudaMemset(h->trace, 0, tb);
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         hsnct_destroy(h);
@@ -323,6 +335,7 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.twiddle);
     cudaFree(h->t.status);
     cudaFree(h->t.counter);
+    cudaFree(h->trace);
     if (h->status_host) cudaFreeHost(h->status_host);
     delete h;
 }
@@ -498,5 +511,19 @@ hsnct_status hsnct_sync(hsnct_t h, void* stream) {
 }
 
 uint64_t hsnct_kernel_launches(hsnct_t h) { return h ? h->launches : 0; }
+
+hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_trace: handle is NULL");
+    const size_t avail = h->trace ? (size_t)h->trace_iters * h->nmf.nblk_f * TRACE_SLOTS : 0;
+    const size_t m = std::min(n, avail);
+    if (n_out) *n_out = avail;
+    if (n_cta) *n_cta = h->nmf.nblk_f;
+    if (m == 0) return HSNCT_OK;
+    if (!host) return fail(HSNCT_E_ARG, "debug_trace: host buffer is NULL");
+    DeviceGuard guard(h->device);
+    CK(cudaMemcpy(host, h->trace, m * sizeof(uint64_t), cudaMemcpyDeviceToHost), "debug_trace");
+    return HSNCT_OK;
+}
 
 }  // extern "C"

@@ -46,7 +46,7 @@ struct NmfPlan {
     bool fused;
     bool persist;    // run all iterations in one cooperative launch (fused path)
     int LP;          // lambda pairs per thread
-    int nbuf;        // tile ring depth
+    int nbuf;        // ring slots per compute group
     int PB;          // B partials of the fused kernel (2 per CTA)
     int nby;         // blocks of the Y+ preparation kernel
     int fthreads;    // threads per CTA
@@ -69,7 +69,11 @@ struct NmfWs {
     double* L2H;     // [nbx*DG2*K*K]
     float* Yp;       // [Np*Nkp] Y+ (fused path only)
     double* ypart;   // [nby] ||Y+||^2 partials (fused path only)
+    // diagnostics (hsnct_debug_trace): per-iteration, per-CTA %globaltimer stamps
+    uint64_t* trace = nullptr;  // [trace_iters][nCTA][TRACE_SLOTS] or null
+    int trace_iters = 0;
 };
+constexpr int TRACE_SLOTS = 5;   // iteration start, pass end, barrier 1, D update done, iteration end
 NmfPlan nmf_plan(const Geometry& g, int num_sms);
 bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p);
 size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);
@@ -81,10 +85,10 @@ cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w,
 int nmf_init_launches(const NmfPlan& p);
 // Enqueues one Lee-Seung iteration (nmf_launches_per_iter launches).
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
-                            int64_t ld_y, float* V, float* D, bool first, double* obj2,
+                            int64_t ld_y, float* V, float* D, int it, double* obj2,
                             unsigned* status, unsigned* counter, cudaStream_t s);
 cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
-                             bool first, unsigned* status, cudaStream_t s);
+                             int it, unsigned* status, cudaStream_t s);
 // All n_iter iterations in one cooperative launch (fused path); bar = 2 zeroed words.
 cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
                                double* obj, unsigned* bar, unsigned* status, cudaStream_t s);

@@ -609,11 +609,12 @@ cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w,
 
 template <int K>
 static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
-                          int64_t ld, float* V, float* D, bool first, double* obj2,
+                          int64_t ld, float* V, float* D, int it, double* obj2,
                           unsigned* status, unsigned* counter, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
+    const bool first = it == 0;
     if (p.fused) {
-        cudaError_t e = nmf_fused_launch(g, p, w, V, D, first, status, s);
+        cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
     } else {
         static bool attr_done = false;  // per-K instantiation
@@ -640,12 +641,12 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
 int nmf_launches_per_iter(const NmfPlan& p) { return p.fused ? 2 : 3; }
 
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
-                            int64_t ld_y, float* V, float* D, bool first, double* obj2,
+                            int64_t ld_y, float* V, float* D, int it, double* obj2,
                             unsigned* status, unsigned* counter, cudaStream_t s) {
     switch (g.K) {
 #define M(KV) \
     case KV:  \
-        return iter_k<KV>(g, p, w, Y, ld_y, V, D, first, obj2, status, counter, s);
+        return iter_k<KV>(g, p, w, Y, ld_y, V, D, it, obj2, status, counter, s);
         HSNCT_K_CASES(M)
 #undef M
         default:

@@ -3,11 +3,10 @@
 
 namespace hsnct {
 
+// Ring slots per compute group: 3 when they fit the shared-memory budget, else 2.
 static int nbuf_for(int Nkp, int LP, int K) {
-    const size_t tile = ((size_t)RG * Nkp + RG * K) * sizeof(float);
-    const size_t fixed = (size_t)(2 * TG * LP) * sizeof(float) * (1 + K);
-    for (int nb = 8; nb >= 4; nb -= 2)   // even: reducer g refills only group-g tiles
-        if (nb * tile + fixed <= 205 * 1024) return nb;
+    for (int nb = 3; nb >= 2; --nb)
+        if (fused_smem_bytes(Nkp, K, LP, nb) <= 212 * 1024) return nb;
     return 0;
 }
 
@@ -18,16 +17,16 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int LP = (pairs + TG - 1) / TG;
     if (LP > lp_cap(g.K)) return false;
     const int nbuf = nbuf_for(Nkp, LP, g.K);
-    if (nbuf < 4) return false;
+    if (nbuf < 2) return false;
     p->LP = LP;
     p->nbuf = nbuf;
     p->fthreads = NTHREADS;
-    p->smem_f = ((size_t)nbuf * (RG * Nkp + RG * g.K) + (size_t)2 * TG * LP * (1 + g.K)) * sizeof(float);
+    p->smem_f = fused_smem_bytes(Nkp, g.K, LP, nbuf);
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const int64_t ntiles = (Np + RG - 1) / RG;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));
     p->PB = p->nblk_f;
-    p->nby = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (Np * (Nkp / 4) + 255) / 256));
+    p->nby = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (Np + 7) / 8));
     return true;
 }
 
@@ -41,10 +40,10 @@ cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w
 #define HSNCT_K8(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
 
 cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
-                             bool first, unsigned* status, cudaStream_t s) {
+                             int it, unsigned* status, cudaStream_t s) {
     switch (g.K) {
 #define M(KV) \
-    case KV: return fused_launch_k<KV>(g, p, w, V, D, first, status, s);
+    case KV: return fused_launch_k<KV>(g, p, w, V, D, it, status, s);
         HSNCT_K8(M)
 #undef M
         default: return cudaErrorInvalidValue;

@@ -1,25 +1,32 @@
-// Fused single-pass Lee-Seung iteration: one read of Y+ per iteration.
+// Fused single-pass Lee-Seung iteration (Eq. 4; R1-R3):
+// one read of Y+ per iteration serves both contractions.
 //
 // Input is Y+ = max(Y, 0) materialised once per decompose call by k_yplus
 // (compact rows of Nkp floats, zero padding), so the hot loop carries no clamp,
-// mask or branch.  One persistent CTA per SM streams 8-row tiles through a ring
-// of NBUF shared-memory buffers filled by cp.async.bulk (one bulk copy per tile,
-// completion on an mbarrier).  The CTA is warp-specialised:
+// mask or ld.  One persistent CTA per SM; CTA c owns the 4-row tiles
+// c, c + nCTA, c + 2 nCTA, ... (a static schedule, identical every iteration),
+// visited forward in even iterations and backward in odd ones, so the tiles a CTA
+// finishes an iteration with -- the ones most likely still in L2 -- are the first
+// it reads in the next.
 //
-//   compute warps  2 groups x 4 warps.  Group g owns rows 4g..4g+3 of every tile;
-//                  thread t of a group owns the lambda pairs 2(t + 128 i), i < LP, for
-//                  the whole kernel, with the matching columns of the CTA's partial
-//                  B = V^T Y+ in registers.
-//                    phase 1 (tile j):   part[r][k] = sum_l Y+[r][l] D[k][l] (D from smem)
-//                                        -> warp transpose-reduce -> red[], arrive part
-//                    phase 2 (tile j-1): B[k][l] += V_new[r][k] Y+[r][l]     -> arrive empty
-//   reducer warp   per tile: fixed-order sum of the 4 warp partials of each row,
-//                  V[r][k] <- V[r][k] A[r][k] / max(sum_j V[r][j] G[j][k], 1e-30),
-//                  H += V_new^T V_new, <V_new, A>; arrive vn; then refills the ring.
-//
-// The V update of tile j overlaps phase 2 of tile j-1, so the compute warps never
-// wait on it.  Per-CTA partials (B per group, H, <V_new, A>) are reduced in a fixed
-// order by k_dred.  Deterministic: static schedule, fixed reduction trees.
+// The CTA is NGRP = 3 compute groups of 4 warps.  Group g takes every third tile
+// of the CTA's sequence and runs its own pipeline:
+//   * its tiles arrive by cp.async.bulk (4 Y+ rows + the 4 old V rows, one
+//     mbarrier per ring slot, NBG slots per group); the last warp to release a slot
+//     refills it, so no thread ever waits to issue a copy;
+//   * thread t of the group owns the lambda pairs 2(t + 128 i), i < LP, for the
+//     whole kernel, with the matching columns of the group's partial B = V^T Y+ in
+//     registers;
+//   * phase 1: part[r][k] = sum_l Y+[r][l] D[k][l] (D from smem, packed f32x2 FMA
+//     when registers allow), warp transpose-reduce -> smem; named barrier;
+//     warp 0 sums the 4 warp partials in a fixed order and updates
+//     V[r][k] <- V[r][k] A[r][k] / max(sum_j V[r][j] G[j][k], 1e-30); named barrier;
+//     warp 0 stores V and accumulates <V_new, A>, warp 1 accumulates H += V_new^T V_new
+//     (fp64); phase 2: B[k][l] += V_new[r][k] Y+[r][l] (packed f32x2 FMA).
+// While one group sits in its V-update barrier the other two keep the SM's four
+// schedulers busy.  Per-CTA partials (B: groups combined in the fixed order
+// (g0 + g1) + g2; H; <V_new, A>) are reduced in a fixed order by the D update.
+// Deterministic: static schedule, fixed reduction trees, no floating-point atomics.
 #pragma once
 #include <algorithm>
 
@@ -28,12 +35,19 @@
 namespace hsnct {
 namespace {
 
-constexpr int RG = 4;              // rows per tile (= rows per compute-group step)
-constexpr int NG = 2;              // compute groups (alternate tiles)
-constexpr int GW = 4;              // warps per group
-constexpr int CW = NG * GW;        // compute warps
+constexpr int RG = 4;              // rows per tile
+#ifndef HSNCT_NGRP
+#define HSNCT_NGRP 3
+#endif
+#ifndef HSNCT_GW
+#define HSNCT_GW 4
+#endif
+constexpr int NGRP = HSNCT_NGRP;   // compute groups
+constexpr int GW = HSNCT_GW;       // warps per group
 constexpr int TG = GW * 32;        // threads per group
-constexpr int NTHREADS = (CW + NG) * 32;   // + one reducer/producer warp per group
+constexpr int NTHREADS = NGRP * TG;
+constexpr int VWARP = GW - 1;      // warp of a group that stores V (fewest lambda pairs)
+constexpr int HWARP = GW - 2;      // warp of a group that accumulates H
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -44,9 +58,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
@@ -64,15 +75,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
-// Orders this thread's prior generic-proxy shared-memory accesses (ring reads)
-// before its subsequent bulk copies into the same buffers.
+// Orders this thread's (and, after a barrier, the CTA's) generic-proxy shared-memory
+// accesses before its subsequent bulk copies into the same buffers.
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// Generic -> async proxy ordering for global memory (V rows written by the
-// previous iteration are read by this iteration's bulk copies).
+// Generic -> async proxy ordering for global memory (V rows written by one
+// iteration are read by the next iteration's bulk copies).
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// d = a * b + c on both halves (one packed FFMA2 on sm_100a), each half rounded
+// exactly like fmaf.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -139,39 +167,44 @@ __device__ __forceinline__ int tr_base(int lane) {
 }
 
 // Y+ = max(Y, 0) into compact rows of Nkp floats (padding = 0); flags non-finite
-// Y (the clamp would hide NaN); per-block ||Y+||^2 partials (fp64).
+// Y (the clamp would hide NaN); per-block ||Y+||^2 partials (fp64).  One warp per
+// row at a time, lanes over lambda quads.
 __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int64_t ld, int64_t Np, int Nk,
                                                int Nkp, float* __restrict__ Yp, double* __restrict__ ypart,
                                                unsigned* __restrict__ status) {
     __shared__ double red[8];
     const int nq = Nkp >> 2;
-    const int64_t total = Np * nq;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * 8;
     double s = 0.0;
     unsigned bad = 0;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = idx / nq;
-        const int q = (int)(idx - p * nq);
-        const int l0 = 4 * q;
-        float4 y = __ldcs(reinterpret_cast<const float4*>(Y + p * ld + l0));
-        if (l0 + 3 >= Nk) {
-            if (l0 + 0 >= Nk) y.x = 0.f;
-            if (l0 + 1 >= Nk) y.y = 0.f;
-            if (l0 + 2 >= Nk) y.z = 0.f;
-            if (l0 + 3 >= Nk) y.w = 0.f;
+    for (int64_t p = (int64_t)blockIdx.x * 8 + w; p < Np; p += nw) {
+        const float4* src = reinterpret_cast<const float4*>(Y + p * ld);
+        float4* dst = reinterpret_cast<float4*>(Yp + p * Nkp);
+        float rs = 0.f;
+#pragma unroll 4
+        for (int q = lane; q < nq; q += 32) {
+            float4 y = __ldcs(src + q);
+            const int l0 = 4 * q;
+            if (l0 + 3 >= Nk) {
+                if (l0 + 0 >= Nk) y.x = 0.f;
+                if (l0 + 1 >= Nk) y.y = 0.f;
+                if (l0 + 2 >= Nk) y.z = 0.f;
+                if (l0 + 3 >= Nk) y.w = 0.f;
+            }
+            if (!(isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w))) bad = ST_Y_NONFINITE;
+            y.x = fmaxf(y.x, 0.f);
+            y.y = fmaxf(y.y, 0.f);
+            y.z = fmaxf(y.z, 0.f);
+            y.w = fmaxf(y.w, 0.f);
+            rs = fmaf(y.x, y.x, fmaf(y.y, y.y, fmaf(y.z, y.z, fmaf(y.w, y.w, rs))));
+            dst[q] = y;
         }
-        if (!(isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w))) bad = ST_Y_NONFINITE;
-        y.x = fmaxf(y.x, 0.f);
-        y.y = fmaxf(y.y, 0.f);
-        y.z = fmaxf(y.z, 0.f);
-        y.w = fmaxf(y.w, 0.f);
-        s += (double)(y.x * y.x + y.y * y.y) + (double)(y.z * y.z + y.w * y.w);
-        reinterpret_cast<float4*>(Yp + p * Nkp)[q] = y;
+        s += (double)rs;
     }
     s = warp_sum_d(s);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (lane == 0) {
         red[w] = s;
         if (bad) atomicOr(status, bad);
@@ -179,341 +212,413 @@ __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int6
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+        for (int i = 0; i < 8; ++i) t += red[i];
         ypart[blockIdx.x] = t;
     }
 }
 
-template <int K, int LP, int NBUF>
+template <int K, int NBG>
 struct FusedShared {
     static constexpr int GK = RG * K;
     static constexpr int KP = (K + 3) & ~3;
     static constexpr int KK = K * K;
-    uint64_t full[NBUF], empty[NBUF], partb[NG], vnb[NG];
-    float red[NG][GW][GK];
-    __align__(16) float Vn[NG][RG][KP];
+    uint64_t full[NGRP][NBG];
+    unsigned rel[NGRP][NBG];
+    float red[NGRP][2][GW][GK];               // per-warp row partials, by tile parity
+    __align__(16) float Vn[NGRP][GW][RG][KP];  // each warp's copy of the tile's new V rows
     float Gs[KK];
-    double hs[NG][KK];
-    double vs[NG];
+    double hs[NGRP][KK];
+    double vs[NGRP];
     unsigned bad;
 };
 
-// One pass over this CTA's tiles (tile j = blockIdx.x + j*gridDim.x, RG rows each)
-// with the current D (smem Ds) and G (sh.Gs).  Tiles alternate between the two
-// compute groups; a group runs phase 1, waits for its reducer warp's V update of
-// that tile, runs phase 2 and releases the buffer while the other group computes.
-// On return (all threads), the CTA's partials are written: B (groups combined in a
-// fixed order) to Bout[K][Nkp], H to Hout[K*K], <V_new, A> to *vout.
-template <int K, int LP, int NBUF>
-__device__ __forceinline__ void tile_pass(const float* __restrict__ Yp, int64_t Np, int Nkp,
-                                          float* __restrict__ V, float* ring, const float* Ds,
-                                          FusedShared<K, LP, NBUF>& sh, float* __restrict__ Bout,
-                                          double* __restrict__ Hout, double* __restrict__ vout,
-                                          bool first) {
-    constexpr int GK = RG * K;
-    constexpr int KP = (K + 3) & ~3;
-    constexpr int DS = 2 * TG * LP;
-    constexpr int KK = K * K;
-    // keep the tile in registers between the phases when it fits the 168-register budget
-    constexpr bool YREG = (2 * RG * LP + 2 * K * LP + RG * K) <= 120;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntiles = (Np + RG - 1) / RG;
-    const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const size_t tile_floats = (size_t)RG * Nkp + RG * K;  // Y+ rows, then the old V rows
+// Dynamic shared memory layout (floats):
+//   ring  [NGRP][NBG][tile]  tile = RG*Nkp Y+ values + RG*K old V values; between
+//                            passes (no copy in flight) it is the group-combine scratch
+//   Ds    [Nkp][KD]          D transposed (lambda-major, KD = K rounded up to even, zero
+//                            padded), in 16-byte chunks swizzled per lambda pair (ds_index)
+//   Bsl   [SCR/2] doubles    the CTA's lambda slice of B in the D update
+// No thread reads past column Nkp of a row (the last lambda pair is guarded).
+constexpr int SCR = 8 * 64;
+__host__ __device__ constexpr size_t tile_floats_of(int Nkp, int K) { return (size_t)RG * Nkp + (size_t)RG * K; }
 
-    if (tid == 0) {
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(&sh.full[b], 1);
-            mbar_init(&sh.empty[b], TG);
-        }
-        for (int g = 0; g < NG; ++g) {
-            mbar_init(&sh.partb[g], TG);
-            mbar_init(&sh.vnb[g], 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+// D in shared memory, lambda-major: the 2*KD values of lambda pair p (D[0..KD)[2p],
+// D[0..KD)[2p+1]) are C = KD/2 consecutive 16-byte chunks, chunk j stored at slot
+// j ^ swz(p).  A thread reads its pair's chunks with LDS.128; the XOR swizzle makes the 8
+// lanes of each quarter-warp hit distinct 16-byte bank groups when C is even (odd C is
+// conflict-free as is).
+template <int K>
+struct DLayout {
+    static constexpr int KD = (K + 1) & ~1;
+    static constexpr int C = KD / 2;   // float4 chunks per lambda pair
+    __host__ __device__ static constexpr int swz(int p) {
+        return C == 2 ? ((p >> 2) & 1) : (C == 4 ? ((p >> 1) & 3) : 0);
     }
-    __syncthreads();
+    // float index of D[k][l] (k < KD)
+    __device__ static __forceinline__ int index(int l, int k) {
+        const int p = l >> 1, f = (l & 1) * KD + k;
+        return ((p * C + ((f >> 2) ^ swz(p))) << 2) + (f & 3);
+    }
+};
 
-    float2 bacc[K][LP];
-    if (warp < CW) {
-        // ======================= compute warps =======================
-        const int g = warp / GW;
-        const int wg = warp - g * GW;
-        const int t = tid - g * TG;
+template <int K, int LP, int NBG>
+struct Pass {
+    static constexpr int GK = RG * K;
+    static constexpr int KP = (K + 3) & ~3;
+    static constexpr int KK = K * K;
+    static constexpr int DS = 2 * TG * LP;
+    using Sh = FusedShared<K, NBG>;
+
+    const float* __restrict__ Yp;
+    int64_t Np;
+    int Nkp;
+    float* __restrict__ V;
+    float* ring;
+    const float* Ds;
+    Sh& sh;
+    int64_t nmine;   // tiles of this CTA
+    size_t tf;       // floats per tile
+
+    __device__ __forceinline__ int64_t count_g(int g) const {
+        return nmine > g ? (nmine - 1 - g) / NGRP + 1 : 0;
+    }
+    __device__ __forceinline__ int64_t row0(int64_t q, bool fwd) const {
+        const int64_t pos = fwd ? q : (nmine - 1 - q);
+        return ((int64_t)blockIdx.x + pos * (int64_t)gridDim.x) * RG;
+    }
+    // Issue the group-g tile with running group counter n and sequence index q.
+    __device__ __forceinline__ void issue(int g, int64_t n, int64_t q, bool fwd) const {
+        const int b = (int)(n % NBG);
+        const int64_t r0 = row0(q, fwd);
+        const int nv = (int)min((int64_t)RG, Np - r0);
+        const unsigned bytes = (unsigned)(nv * Nkp * sizeof(float));
+        const unsigned vbytes = nv == RG ? (unsigned)(RG * K * sizeof(float)) : 0u;  // 16K bytes
+        uint64_t* bar = &sh.full[g][b];
+        mbar_expect_tx(bar, bytes + vbytes);
+        float* slot = ring + (size_t)(g * NBG + b) * tf;
+        bulk_g2s(slot, Yp + r0 * Nkp, bytes, bar);
+        if (vbytes) bulk_g2s(slot + (size_t)RG * Nkp, V + r0 * K, vbytes, bar);
+    }
+    // Leader of group g: the first NBG tiles of a pass (counter base n0).
+    __device__ __forceinline__ void issue_head(int g, int64_t n0, bool fwd) const {
+        const int64_t c = count_g(g);
+        for (int64_t m = 0; m < min((int64_t)NBG, c); ++m) issue(g, n0 + m, g + (int64_t)NGRP * m, fwd);
+    }
+
+    // One pass over this CTA's tiles with the current D (Ds) and G (sh.Gs).
+    // n0: running group tile counter at the start of the pass (mbarrier phases).
+    // If !prefetched the pass issues its own head tiles; if next >= 0 the head tiles
+    // of the next pass (direction next_fwd) are issued once this pass is done.
+    // On return (all threads): Bout[K][Nkp], Hout[KK], *vout written.
+    __device__ void run(int64_t n0, bool first, bool fwd, bool prefetched, bool prefetch_next, bool next_fwd,
+                        float* __restrict__ Bout, double* __restrict__ Hout, double* __restrict__ vout) const {
+        const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+        const int g = warp / GW, wg = warp - g * GW, t = tid - g * TG;
+        const int64_t cnt = count_g(g);
+        if (!prefetched) {
+            if (t == 0) {
+                fence_proxy_async_global();
+                fence_proxy_async();
+                issue_head(g, n0, fwd);
+            }
+        }
+        const bool lastok = 2 * (t + TG * (LP - 1)) < Nkp;  // last lambda pair inside the row
+        float2 bacc[K][LP];
 #pragma unroll
         for (int k = 0; k < K; ++k)
 #pragma unroll
             for (int i = 0; i < LP; ++i) bacc[k][i] = make_float2(0.f, 0.f);
-        const float* dbase = Ds + 2 * t;
-        int64_t kth = 0;  // this group's tile count
-        for (int64_t j = g; j < nmine; j += NG, ++kth) {
-            const int b = (int)(j % NBUF);
-            mbar_wait(&sh.full[b], (unsigned)((j / NBUF) & 1));
-            const float* yb = ring + (size_t)b * tile_floats + 2 * t;
-            // YREG: the tile's Y+ values owned by this thread go to registers and the
-            // buffer is released at once (deeper prefetch, phase 2 without smem reads);
-            // otherwise phase 2 re-reads the buffer and releases it afterwards.
-            float2 y[YREG ? LP : 1][RG];
-            if constexpr (YREG) {
-#pragma unroll
-                for (int i = 0; i < LP; ++i)
-#pragma unroll
-                    for (int r = 0; r < RG; ++r)
-                        y[i][r] = *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i);
-                mbar_arrive(&sh.empty[b]);
-            }
-            // ---- phase 1
-            float part[GK];
-#pragma unroll
-            for (int x = 0; x < GK; ++x) part[x] = 0.f;
-#pragma unroll
-            for (int i = 0; i < LP; ++i) {
-                float2 yy[RG];
-#pragma unroll
-                for (int r = 0; r < RG; ++r)
-                    yy[r] = YREG ? y[YREG ? i : 0][r]
-                                 : *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i);
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float2 d = *reinterpret_cast<const float2*>(dbase + k * DS + 2 * TG * i);
-#pragma unroll
-                    for (int r = 0; r < RG; ++r)
-                        part[r * K + k] = fmaf(yy[r].x, d.x, fmaf(yy[r].y, d.y, part[r * K + k]));
-                }
-            }
-            tr_step<16, GK>(part, lane);
-            if (((unsigned)lane & tr_bfly(GK)) == 0) {
-                const int base = tr_base<GK>(lane);
-#pragma unroll
-                for (int x = 0; x < tr_nout(GK); ++x) sh.red[g][wg][base + x] = part[x];
-            }
-            mbar_arrive(&sh.partb[g]);
-            // ---- phase 2 (after the reducer's V update of this tile)
-            mbar_wait(&sh.vnb[g], (unsigned)(kth & 1));
-#pragma unroll
-            for (int r = 0; r < RG; ++r) {
-                float vr[KP];
-#pragma unroll
-                for (int q = 0; q < KP / 4; ++q) {
-                    const float4 v4 = reinterpret_cast<const float4*>(&sh.Vn[g][r][0])[q];
-                    vr[4 * q + 0] = v4.x;
-                    vr[4 * q + 1] = v4.y;
-                    vr[4 * q + 2] = v4.z;
-                    vr[4 * q + 3] = v4.w;
-                }
-#pragma unroll
-                for (int i = 0; i < LP; ++i) {
-                    const float2 yv = YREG ? y[YREG ? i : 0][r]
-                                           : *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        bacc[k][i].x = fmaf(vr[k], yv.x, bacc[k][i].x);
-                        bacc[k][i].y = fmaf(vr[k], yv.y, bacc[k][i].y);
-                    }
-                }
-            }
-            if constexpr (!YREG) mbar_arrive(&sh.empty[b]);
-        }
-    } else {
-        // =============== reducer / producer warp of group g (tiles j = g mod NG) ===============
-        const int g = warp - CW;
-        auto issue = [&](int64_t jj) {
-            const int b = (int)(jj % NBUF);
-            const int64_t r0 = (blockIdx.x + jj * gridDim.x) * RG;
-            const int nv = (int)min((int64_t)RG, Np - r0);
-            const unsigned bytes = (unsigned)(nv * Nkp * sizeof(float));
-            const unsigned vbytes = nv == RG ? (unsigned)(RG * K * sizeof(float)) : 0u;  // 16K bytes
-            mbar_expect_tx(&sh.full[b], bytes + vbytes);
-            float* slot = ring + (size_t)b * tile_floats;
-            bulk_g2s(slot, Yp + r0 * Nkp, bytes, &sh.full[b]);
-            if (vbytes) bulk_g2s(slot + (size_t)RG * Nkp, V + r0 * K, vbytes, &sh.full[b]);
-        };
-        if (lane == 0) {
-            fence_proxy_async_global();
-            fence_proxy_async();
-            for (int64_t jj = g; jj < min((int64_t)NBUF, nmine); jj += NG) issue(jj);
-        }
+        using DL = DLayout<K>;
+        constexpr int KD = DL::KD, C = DL::C;
         double vdotA = 0.0;
         double hacc[(KK + 31) / 32];
 #pragma unroll
         for (int x = 0; x < (KK + 31) / 32; ++x) hacc[x] = 0.0;
         unsigned bad = 0;
-        int64_t kth = 0;
-        for (int64_t j = g; j < nmine; j += NG, ++kth) {
-            const int64_t r0 = (blockIdx.x + j * gridDim.x) * RG;
+        for (int64_t m = 0; m < cnt; ++m) {
+            const int64_t n = n0 + m;
+            const int b = (int)(n % NBG);
+            const int64_t q = g + (int64_t)NGRP * m;
+            const int64_t r0 = row0(q, fwd);
             const int nv = (int)min((int64_t)RG, Np - r0);
-            const int b = (int)(j % NBUF);
-            mbar_wait(&sh.full[b], (unsigned)((j / NBUF) & 1));
-            const float* vslot = ring + (size_t)b * tile_floats + (size_t)RG * Nkp;
-            float vo_all[(GK + 31) / 32][K];
-            float vo_me[(GK + 31) / 32];
+            mbar_wait(&sh.full[g][b], (unsigned)((n / NBG) & 1));
+            const float* slot = ring + (size_t)(g * NBG + b) * tf;
+            const float* yb = slot + 2 * t;
+            // ---- V-update factor V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old
+            //      V rows (lane s -> (r, k)); independent of phase 1, so its latency hides
+            float rfac = 0.f, vome = 0.f;
+            if (lane < GK) {
+                const int r = lane / K, k = lane - (lane / K) * K;
+                const float* vslot = slot + (size_t)RG * Nkp;
+                float vg = 0.f;
 #pragma unroll
-            for (int u = 0; u < (GK + 31) / 32; ++u) {
-                const int s = lane + 32 * u;
-                const int r = (s < GK ? s : 0) / K;
-#pragma unroll
-                for (int jj = 0; jj < K; ++jj)
-                    vo_all[u][jj] = nv == RG ? vslot[r * K + jj] : ((r < nv) ? V[(r0 + r) * K + jj] : 0.f);
-                vo_me[u] = vo_all[u][s < GK ? s - r * K : 0];
+                for (int j = 0; j < K; ++j) {
+                    const float vj = nv == RG ? vslot[r * K + j] : ((r < nv) ? V[(r0 + r) * K + j] : 0.f);
+                    vg = fmaf(vj, sh.Gs[j * K + k], vg);
+                    if (j == k) vome = vj;
+                }
+                rfac = __fdiv_rn(vome, fmaxf(vg, 1e-30f));
             }
-            mbar_wait(&sh.partb[g], (unsigned)(kth & 1));
-            float vnew[(GK + 31) / 32], aval[(GK + 31) / 32];
+            // ---- phase 1: row partials of A = Y+ D^T over this thread's lambda pairs
+            // p2[r][kp] = (A[r][2kp], A[r][2kp+1]) partials; per lambda one packed FFMA2
+            // per (r, k pair) with Y+[r][lambda] broadcast and (D[2kp][l], D[2kp+1][l])
+            float2 p2[RG][KD / 2];
 #pragma unroll
-            for (int u = 0; u < (GK + 31) / 32; ++u) {
-                const int s = lane + 32 * u;
-                vnew[u] = 0.f;
-                aval[u] = 0.f;
+            for (int r = 0; r < RG; ++r)
+#pragma unroll
+                for (int kp = 0; kp < KD / 2; ++kp) p2[r][kp] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < LP; ++i) {
+                const bool ok = (i < LP - 1) || lastok;
+                const int pp = t + TG * i;  // lambda pair
+                float2 yy[RG];
+#pragma unroll
+                for (int r = 0; r < RG; ++r)
+                    yy[r] = ok ? *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i)
+                               : make_float2(0.f, 0.f);
+                float dd[2 * KD];
+#pragma unroll
+                for (int j = 0; j < C; ++j) {
+                    const float4 q4 = ok ? reinterpret_cast<const float4*>(Ds)[pp * C + (j ^ DL::swz(pp))]
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                    dd[4 * j + 0] = q4.x;
+                    dd[4 * j + 1] = q4.y;
+                    dd[4 * j + 2] = q4.z;
+                    dd[4 * j + 3] = q4.w;
+                }
+#pragma unroll
+                for (int r = 0; r < RG; ++r)
+#pragma unroll
+                    for (int kp = 0; kp < KD / 2; ++kp) {
+                        p2[r][kp] = ffma2(make_float2(yy[r].x, yy[r].x), make_float2(dd[2 * kp], dd[2 * kp + 1]),
+                                          p2[r][kp]);
+                        p2[r][kp] = ffma2(make_float2(yy[r].y, yy[r].y),
+                                          make_float2(dd[KD + 2 * kp], dd[KD + 2 * kp + 1]), p2[r][kp]);
+                    }
+            }
+            float part[GK];
+#pragma unroll
+            for (int r = 0; r < RG; ++r)
+#pragma unroll
+                for (int k = 0; k < K; ++k) part[r * K + k] = (k & 1) ? p2[r][k >> 1].y : p2[r][k >> 1].x;
+            tr_step<16, GK>(part, lane);
+            const int par = (int)(m & 1);
+            if (((unsigned)lane & tr_bfly(GK)) == 0) {
+                const int base = tr_base<GK>(lane);
+#pragma unroll
+                for (int x = 0; x < tr_nout(GK); ++x) sh.red[g][par][wg][base + x] = part[x];
+            }
+            named_bar(1 + g, TG);
+            // ---- V update, redundantly in every warp (lane s -> (r, k)): no second barrier
+            {
+                const int s = lane;
                 if (s < GK) {
-                    const int r = s / K, k = s - (s / K) * K;
                     float a = 0.f;
 #pragma unroll
-                    for (int w = 0; w < GW; ++w) a += sh.red[g][w][s];
-                    float vg = 0.f;
-#pragma unroll
-                    for (int jj = 0; jj < K; ++jj) vg = fmaf(vo_all[u][jj], sh.Gs[jj * K + k], vg);
-                    float vn = __fdiv_rn(vo_me[u] * a, fmaxf(vg, 1e-30f));
-                    if (r >= nv) vn = 0.f;
-                    vnew[u] = vn;
-                    aval[u] = a;
-                    sh.Vn[g][r][k] = vn;
+                    for (int w = 0; w < GW; ++w) a += sh.red[g][par][w][s];
+                    float vn = a * rfac;
+                    if (s / K >= nv) vn = 0.f;
+                    sh.Vn[g][wg][s / K][s - (s / K) * K] = vn;
+                    if (wg == VWARP && s / K < nv) {
+                        if (first && !(isfinite(vome) && vome >= 0.f)) bad |= ST_INIT_BAD;
+                        if (!isfinite(vn)) bad |= ST_NUMERIC;
+                        V[r0 * K + s] = vn;
+                        vdotA += (double)vn * (double)a;
+                    }
                 }
             }
             __syncwarp();
-            mbar_arrive(&sh.vnb[g]);
-            // off the compute warps' critical path: V store, checks, objective, H, refill
+            if (wg == HWARP) {
 #pragma unroll
-            for (int u = 0; u < (GK + 31) / 32; ++u) {
-                const int s = lane + 32 * u;
-                if (s < GK && s / K < nv) {
-                    if (first && !(isfinite(vo_me[u]) && vo_me[u] >= 0.f)) bad |= ST_INIT_BAD;
-                    if (!isfinite(vnew[u])) bad |= ST_NUMERIC;
-                    V[r0 * K + s] = vnew[u];
-                    vdotA += (double)vnew[u] * (double)aval[u];
+                for (int x = 0; x < (KK + 31) / 32; ++x) {
+                    const int tt = lane + 32 * x;
+                    if (tt < KK) {
+                        const int a = tt / K, c = tt - (tt / K) * K;
+                        double s = 0.0;
+#pragma unroll
+                        for (int r = 0; r < RG; ++r)
+                            s = fma((double)sh.Vn[g][wg][r][a], (double)sh.Vn[g][wg][r][c], s);
+                        hacc[x] += s;
+                    }
                 }
             }
+            // ---- phase 2: B[k][l] += V_new[r][k] Y+[r][l]
+#pragma unroll
+            for (int r = 0; r < RG; ++r) {
+                float vr[KP];
+#pragma unroll
+                for (int qq = 0; qq < KP / 4; ++qq) {
+                    const float4 v4 = reinterpret_cast<const float4*>(&sh.Vn[g][wg][r][0])[qq];
+                    vr[4 * qq + 0] = v4.x;
+                    vr[4 * qq + 1] = v4.y;
+                    vr[4 * qq + 2] = v4.z;
+                    vr[4 * qq + 3] = v4.w;
+                }
+#pragma unroll
+                for (int i = 0; i < LP; ++i) {
+                    const bool ok = (i < LP - 1) || lastok;
+                    const float2 yv = ok ? *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i)
+                                         : make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < K; ++k) bacc[k][i] = ffma2(make_float2(vr[k], vr[k]), yv, bacc[k][i]);
+                }
+            }
+            // ---- release the slot; the last warp out refills it with tile m + NBG
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                // monotone counter: every use of a slot adds GW, so the last warp of a
+                // use sees old % GW == GW - 1 (no reset, no race with the next use)
+                if (atomicAdd(&sh.rel[g][b], 1u) % GW == GW - 1) {
+                    if (m + NBG < cnt) {
+                        fence_proxy_async();
+                        issue(g, n + NBG, q + (int64_t)NGRP * NBG, fwd);
+                    }
+                }
+            }
+        }
+        // ---- per-group partials to smem
+        if (wg == VWARP) {
+            vdotA = warp_sum_d(vdotA);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+            if (lane == 0) {
+                sh.vs[g] = vdotA;
+                if (bad) atomicOr(&sh.bad, bad);
+            }
+        } else if (wg == HWARP) {
 #pragma unroll
             for (int x = 0; x < (KK + 31) / 32; ++x) {
                 const int tt = lane + 32 * x;
-                if (tt < KK) {
-                    const int a = tt / K, c = tt - (tt / K) * K;
-                    double s = 0.0;
-#pragma unroll
-                    for (int r = 0; r < RG; ++r) s = fma((double)sh.Vn[g][r][a], (double)sh.Vn[g][r][c], s);
-                    hacc[x] += s;
-                }
-            }
-            // refill.  YREG: the group released tile j's buffer before arriving on
-            // part(j).  Otherwise: its previous tile j - NG was released before part(j).
-            const int64_t m = YREG ? j : j - NG;
-            if (m >= 0 && m + NBUF < nmine) {
-                mbar_wait(&sh.empty[m % NBUF], (unsigned)((m / NBUF) & 1));
-                if (lane == 0) {
-                    fence_proxy_async();
-                    issue(m + NBUF);
-                }
+                if (tt < KK) sh.hs[g][tt] = hacc[x];
             }
         }
-        vdotA = warp_sum_d(vdotA);
+        __syncthreads();
+        // ---- CTA partial of B: groups added in order, one k at a time through the idle ring
+        float* comb = ring;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-        if (lane == 0) {
-            sh.vs[g] = vdotA;
-            if (bad) atomicOr(&sh.bad, bad);
-        }
+        for (int k = 0; k < K; ++k) {
+            if (g > 0) {
 #pragma unroll
-        for (int x = 0; x < (KK + 31) / 32; ++x) {
-            const int tt = lane + 32 * x;
-            if (tt < KK) sh.hs[g][tt] = hacc[x];
-        }
-    }
-    // ---- CTA partials: group 1's B through smem (the ring is idle now), fixed order 0 + 1
-    __syncthreads();
-    float* scratch = ring;  // [K][DS]
-    if (warp >= GW && warp < CW) {
-        const int t = tid - TG;
+                for (int i = 0; i < LP; ++i)
+                    *reinterpret_cast<float2*>(comb + (g - 1) * DS + 2 * (t + TG * i)) = bacc[k][i];
+            }
+            __syncthreads();
+            if (g == 0) {
 #pragma unroll
-        for (int i = 0; i < LP; ++i)
+                for (int i = 0; i < LP; ++i) {
+                    const int l0 = 2 * (t + TG * i);
+                    if (l0 < Nkp) {
+                        float2 o = bacc[k][i];
 #pragma unroll
-            for (int k = 0; k < K; ++k)
-                *reinterpret_cast<float2*>(scratch + k * DS + 2 * (t + TG * i)) = bacc[k][i];
-    }
-    __syncthreads();
-    if (warp < GW) {
-        const int t = tid;
-#pragma unroll
-        for (int i = 0; i < LP; ++i) {
-            const int l0 = 2 * (t + TG * i);
-            if (l0 < Nkp) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float2 o = *reinterpret_cast<const float2*>(scratch + k * DS + l0);
-                    *reinterpret_cast<float2*>(Bout + (int64_t)k * Nkp + l0) =
-                        make_float2(bacc[k][i].x + o.x, bacc[k][i].y + o.y);
+                        for (int gg = 1; gg < NGRP; ++gg) {
+                            const float2 og = *reinterpret_cast<const float2*>(comb + (gg - 1) * DS + l0);
+                            o.x += og.x;
+                            o.y += og.y;
+                        }
+                        *reinterpret_cast<float2*>(Bout + (int64_t)k * Nkp + l0) = o;
+                    }
                 }
             }
+            __syncthreads();
+        }
+        for (int o = tid; o < KK; o += NTHREADS) {
+            double h = sh.hs[0][o];
+            for (int gg = 1; gg < NGRP; ++gg) h += sh.hs[gg][o];
+            Hout[o] = h;
+        }
+        if (tid == 0) {
+            double v = sh.vs[0];
+            for (int gg = 1; gg < NGRP; ++gg) v += sh.vs[gg];
+            *vout = v;
+        }
+        // ---- head tiles of the next pass (ring idle again; V rows are final)
+        fence_proxy_async_global();  // this thread's V stores before the next bulk copies
+        __syncthreads();
+        if (prefetch_next && t == 0) {
+            fence_proxy_async();
+            issue_head(g, n0 + cnt, next_fwd);
         }
     }
-    for (int o = tid; o < KK; o += NTHREADS) Hout[o] = sh.hs[0][o] + sh.hs[1][o];
-    if (tid == 0) *vout = sh.vs[0] + sh.vs[1];
-    __syncthreads();  // scratch (ring) reads done before any reuse
+};
+
+// Shared prologue: mbarriers, release counters, zeroed ring + slack.
+template <int K, int NBG>
+__device__ __forceinline__ void fused_prologue(FusedShared<K, NBG>& sh, float* ring, size_t ring_floats) {
+    for (size_t i = threadIdx.x; i < ring_floats; i += NTHREADS) ring[i] = 0.f;
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < NGRP; ++g)
+            for (int b = 0; b < NBG; ++b) {
+                mbar_init(&sh.full[g][b], 1);
+                sh.rel[g][b] = 0u;
+            }
+        sh.bad = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_proxy_async();  // zero fill (generic) before the first bulk copies (async)
 }
 
-// Stage D (zero padded to DS columns) and G into shared memory.
-template <int K, int LP, int NBUF>
-__device__ __forceinline__ void stage_dg(const float* __restrict__ D, int Nk, const double* Gsrc, float* Ds,
-                                         FusedShared<K, LP, NBUF>& sh) {
-    constexpr int DS = 2 * TG * LP;
-    for (int i = threadIdx.x; i < K * DS; i += NTHREADS) {
-        const int k = i / DS, l = i - k * DS;
-        Ds[i] = (l < Nk) ? __ldcg(D + (int64_t)k * Nk + l) : 0.f;
+// Stage D (lambda-major, swizzled, zero padded; DLayout) and G into shared memory.
+// Global reads are coalesced (row-major D); the shared-memory writes scatter.
+template <int K>
+__device__ __forceinline__ void stage_dg(const float* __restrict__ D, int Nk, int Nkp, const double* Gsrc, float* Ds,
+                                         float* Gs) {
+    using DL = DLayout<K>;
+    constexpr int KD = DL::KD;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < KD * Nkp; i += NTHREADS) {
+        const int k = i / Nkp, l = i - k * Nkp;
+        Ds[DL::index(l, k)] = (k < K && l < Nk) ? __ldcg(D + (int64_t)k * Nk + l) : 0.f;
     }
-    for (int i = threadIdx.x; i < K * K; i += NTHREADS) sh.Gs[i] = (float)Gsrc[i];
+    for (int i = threadIdx.x; i < K * K; i += NTHREADS) Gs[i] = (float)Gsrc[i];
 }
 
-template <int K, int LP, int NBUF>
+// One iteration's row pass per launch (fallback when a cooperative launch is refused).
+template <int K, int LP, int NBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restrict__ Yp, int64_t Np, int Nk,
                                                            int Nkp, float* __restrict__ V,
                                                            const float* __restrict__ D,
                                                            const double* __restrict__ Gd,
                                                            float* __restrict__ Bpart,
                                                            double* __restrict__ Hpart,
-                                                           double* __restrict__ vpart, int first,
+                                                           double* __restrict__ vpart, int it,
                                                            unsigned* __restrict__ status) {
-    constexpr int DS = 2 * TG * LP;
-    __shared__ FusedShared<K, LP, NBUF> sh;
+    using P = Pass<K, LP, NBG>;
+    constexpr int DS = P::DS;
+    __shared__ FusedShared<K, NBG> sh;
     extern __shared__ __align__(128) float smem[];
-    const size_t tile_floats = (size_t)RG * Nkp + RG * K;
-    float* ring = smem;                              // [NBUF][tile] + slack DS
-    float* Ds = smem + NBUF * tile_floats + DS;      // [K][DS]
-    for (size_t i = threadIdx.x; i < NBUF * tile_floats + DS; i += NTHREADS) ring[i] = 0.f;
-    if (threadIdx.x == 0) sh.bad = 0u;
-    stage_dg<K, LP, NBUF>(D, Nk, Gd, Ds, sh);
+    const size_t tf = tile_floats_of(Nkp, K);
+    const size_t ring_floats = (size_t)NGRP * NBG * tf;
+    float* ring = smem;
+    float* Ds = smem + max(ring_floats, (size_t)(NGRP - 1) * DS);  // the ring doubles as the B-combine scratch
+    fused_prologue<K, NBG>(sh, ring, ring_floats);
+    stage_dg<K>(D, Nk, Nkp, Gd, Ds, sh.Gs);
     __syncthreads();
-    tile_pass<K, LP, NBUF>(Yp, Np, Nkp, V, ring, Ds, sh, Bpart + (int64_t)blockIdx.x * K * Nkp,
-                           Hpart + (int64_t)blockIdx.x * K * K, vpart + 2 * (int64_t)blockIdx.x, first != 0);
+    const int64_t ntiles = (Np + RG - 1) / RG;
+    const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    P pass{Yp, Np, Nkp, V, ring, Ds, sh, nmine, tf};
+    pass.run(0, it == 0, (it & 1) == 0, false, false, false, Bpart + (int64_t)blockIdx.x * K * Nkp,
+             Hpart + (int64_t)blockIdx.x * K * K, vpart + 2 * (int64_t)blockIdx.x);
     if (threadIdx.x == 0) {
         vpart[2 * (int64_t)blockIdx.x + 1] = 0.0;
         if (sh.bad) atomicOr(status, sh.bad);
     }
 }
 
-// Software grid barrier for a cooperative launch (all CTAs co-resident).
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen) {
+// Grid barrier for a cooperative launch (all CTAs co-resident): a monotone arrival
+// counter (zeroed by the host before the launch); barrier number e completes when the
+// counter reaches e * nCTA.  One release-add per CTA, acquire polling, no second atomic.
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned& epoch) {
     __syncthreads();
+    ++epoch;
     if (threadIdx.x == 0) {
-        const unsigned g = *(volatile unsigned*)gen;
         __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            *(volatile unsigned*)count = 0u;
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            unsigned cur;
-            do {
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
-                if (cur == g) __nanosleep(64);
-            } while (cur == g);
-        }
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
+        const unsigned target = epoch * gridDim.x;
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(count) : "memory");
+        } while ((int)(cur - target) < 0);
         __threadfence();
     }
     __syncthreads();
@@ -530,135 +635,180 @@ struct PersistArgs {
     double* Hpart;   // [nCTA][KK]
     double* vpart;   // [nCTA][2]
     double* dpart;   // [nCTA]
-    double* Gpart;   // [nCTA][KK]
     const double* ypart;
     int nby;
     double* ysq;
     double* obj;     // [2 n_iter] or null
-    unsigned* bar;   // [2] barrier count, generation
+    uint64_t* trace; // [trace_iters][nCTA][TRACE_SLOTS] or null (diagnostics)
+    int trace_iters;
+    unsigned* bar;   // arrival counter, zero at launch
     unsigned* status;
 };
 
+// Fixed-order block reduction of one double per thread, result in every thread.
+__device__ __forceinline__ double block_sum_all(double v, double* sh) {
+    v = warp_sum_d(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+    __syncthreads();
+    return s;
+}
+
 // All n_iter Lee-Seung iterations in one cooperative launch.  Per iteration:
-//   tile_pass -> grid barrier -> D update of this CTA's lambda slice (B, H reduced
-//   over the CTA partials in a fixed order) -> grid barrier -> G_new from the slice
-//   partials (every CTA, same fixed order), objective (CTA 0), D restaged.
-template <int K, int LP, int NBUF>
+//   pass (the next pass's head tiles are issued as soon as it ends) -> grid barrier
+//   -> H and this CTA's lambda slice of B reduced over the CTA partials in a fixed
+//   order (one sweep of loads), D update of the slice, <B, D_new> slice partial ->
+//   grid barrier -> D restaged, G_new = D_new D_new^T from the staged D (every CTA,
+//   same fixed order, fp64), objective (last CTA, which has the fewest tiles).
+template <int K, int LP, int NBG>
 __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
-    constexpr int DS = 2 * TG * LP;
+    using P = Pass<K, LP, NBG>;
+    constexpr int DS = P::DS;
     constexpr int KK = K * K;
-    __shared__ FusedShared<K, LP, NBUF> sh;
+    __shared__ FusedShared<K, NBG> sh;
     __shared__ double Hs[KK], Gold[KK], Gnew[KK];
     __shared__ double gacc[NTHREADS];
-    __shared__ double sc[4];
+    __shared__ double red[NTHREADS / 32];
     extern __shared__ __align__(128) float smem[];
     const int tid = threadIdx.x;
     const int nC = gridDim.x, c = blockIdx.x;
-    const size_t tile_floats = (size_t)RG * A.Nkp + RG * K;
+    const size_t tf = tile_floats_of(A.Nkp, K);
+    const size_t ring_floats = (size_t)NGRP * NBG * tf;
     float* ring = smem;
-    float* Ds = smem + NBUF * tile_floats + DS;
-    for (size_t i = tid; i < NBUF * tile_floats + DS; i += NTHREADS) ring[i] = 0.f;
+    float* Ds = smem + max(ring_floats, (size_t)(NGRP - 1) * DS);  // the ring doubles as the B-combine scratch
+    double* Bsl = reinterpret_cast<double*>(Ds + (size_t)DLayout<K>::KD * A.Nkp);  // [SCR/2] B slice (fp64)
+    fused_prologue<K, NBG>(sh, ring, ring_floats);
     for (int i = tid; i < KK; i += NTHREADS) Gold[i] = A.Gd[i];
-    if (tid == 0) sh.bad = 0u;
-    stage_dg<K, LP, NBUF>(A.D, A.Nk, Gold, Ds, sh);
     __syncthreads();
+    stage_dg<K>(A.D, A.Nk, A.Nkp, Gold, Ds, sh.Gs);
+    __syncthreads();
+    const int64_t ntiles = (A.Np + RG - 1) / RG;
+    const int64_t nmine = ntiles > c ? (ntiles - 1 - c) / nC + 1 : 0;
+    P pass{A.Yp, A.Np, A.Nkp, A.V, ring, Ds, sh, nmine, tf};
+    const int g = tid / TG;
+    const int64_t cnt = pass.count_g(g);
     // lambda slice of this CTA for the D update
     const int SL = (A.Nk + nC - 1) / nC;
-    const int l0 = c * SL, l1 = min(A.Nk, l0 + SL);
+    const int l0 = min(A.Nk, c * SL), l1 = min(A.Nk, l0 + SL);
     const int nsl = max(0, l1 - l0);
+    const bool dvec = (A.Nk % 4 == 0) && ((reinterpret_cast<uintptr_t>(A.D) & 15) == 0);
+    unsigned epoch = 0;
     double ysq = 0.0;
+    int64_t n0 = 0;
+    auto stamp = [&](int it, int slot) {
+        if (A.trace && tid == 0 && it < A.trace_iters) {
+            uint64_t tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            A.trace[((int64_t)it * nC + c) * TRACE_SLOTS + slot] = tnow;
+        }
+    };
     for (int it = 0; it < A.n_iter; ++it) {
-        tile_pass<K, LP, NBUF>(A.Yp, A.Np, A.Nkp, A.V, ring, Ds, sh, A.Bpart + (int64_t)c * K * A.Nkp,
-                               A.Hpart + (int64_t)c * KK, A.vpart + 2 * (int64_t)c, it == 0);
-        grid_sync(A.bar, A.bar + 1);
-        // ---- H = sum_c Hpart[c] (fixed order: residue classes, then classes in order)
+        const bool fwd = (it & 1) == 0;
+        stamp(it, 0);
+        pass.run(n0, it == 0, fwd, it > 0, it + 1 < A.n_iter, !fwd, A.Bpart + (int64_t)c * K * A.Nkp,
+                 A.Hpart + (int64_t)c * KK, A.vpart + 2 * (int64_t)c);
+        n0 += cnt;
+        stamp(it, 1);
+        grid_sync(A.bar, epoch);
+        stamp(it, 2);
+        // ---- H (KK outputs) and the B slice (K x nsl outputs) over the nC partials
         {
-            constexpr int NQ = NTHREADS / KK > 0 ? NTHREADS / KK : 1;
-            if (tid < NQ * KK) {
-                const int o = tid % KK, q = tid / KK;
+            const int nB = K * nsl, nout = KK + nB;
+            const int NQ = max(1, NTHREADS / nout);
+            if (tid < NQ * nout) {
+                const int o = tid % nout, q = tid / nout;
                 double s = 0.0;
-                for (int cc = q; cc < nC; cc += NQ) s += __ldcg(A.Hpart + (int64_t)cc * KK + o);
+                if (o < KK) {
+                    const double* src = A.Hpart + o;
+#pragma unroll 8
+                    for (int cc = q; cc < nC; cc += NQ) s += __ldcg(src + (int64_t)cc * KK);
+                } else {
+                    const int ob = o - KK, k = ob / nsl, l = l0 + (ob - (ob / nsl) * nsl);
+                    const float* src = A.Bpart + (int64_t)k * A.Nkp + l;
+                    const int64_t stride = (int64_t)K * A.Nkp;
+#pragma unroll 8
+                    for (int cc = q; cc < nC; cc += NQ) s += (double)__ldcg(src + (int64_t)cc * stride);
+                }
                 gacc[tid] = s;
             }
             __syncthreads();
-            for (int o = tid; o < KK; o += NTHREADS) {
+            for (int o = tid; o < nout; o += NTHREADS) {
                 double s = 0.0;
-                for (int q = 0; q < NQ; ++q) s += gacc[q * KK + o];
-                Hs[o] = s;
+                for (int q = 0; q < NQ; ++q) s += gacc[q * nout + o];
+                if (o < KK) Hs[o] = s;
+                else Bsl[o - KK] = s;
             }
             __syncthreads();
         }
-        // ---- B for the slice (K x nsl outputs over nC partials), D update, slice partials
+        // ---- D update of the slice, <B, D_new> slice partial (fixed order)
         {
-            const int nout = K * nsl;
-            const int NQ = nout > 0 ? max(1, NTHREADS / nout) : 1;
-            if (nout > 0 && tid < NQ * nout) {
-                const int o = tid % nout, q = tid / nout;
-                const int k = o / nsl, l = l0 + (o - (o / nsl) * nsl);
-                double s = 0.0;
-                for (int cc = q; cc < nC; cc += NQ)
-                    s += (double)__ldcg(A.Bpart + ((int64_t)cc * K + k) * A.Nkp + l);
-                gacc[tid] = s;
-            }
-            __syncthreads();
             double bd = 0.0;
-            float dn[K];
-            unsigned bad = 0;
             if (tid < nsl) {
                 const int l = l0 + tid;
-                double B[K], d[K];
+                unsigned bad = 0;
+                double d[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    double s = 0.0;
-                    for (int q = 0; q < NQ; ++q) s += gacc[q * nout + k * nsl + tid];
-                    B[k] = s;
-                    d[k] = (double)__ldcg(A.D + (int64_t)k * A.Nk + l);
-                }
+                for (int k = 0; k < K; ++k) d[k] = (double)__ldcg(A.D + (int64_t)k * A.Nk + l);
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     double hd = 0.0;
 #pragma unroll
                     for (int jj = 0; jj < K; ++jj) hd = fma(Hs[k * K + jj], d[jj], hd);
-                    dn[k] = (float)(d[k] * B[k] / fmax(hd, 1e-30));
-                    if (!isfinite(dn[k])) bad |= ST_NUMERIC;
-                    bd += B[k] * (double)dn[k];
+                    const double B = Bsl[k * nsl + tid];
+                    const float dn = (float)(d[k] * B / fmax(hd, 1e-30));
+                    if (!isfinite(dn)) bad |= ST_NUMERIC;
+                    bd += B * (double)dn;
+                    A.D[(int64_t)k * A.Nk + l] = dn;
                 }
-            }
-            __syncthreads();  // all reads of the old D slice done
-            if (tid < nsl) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) A.D[(int64_t)k * A.Nk + l0 + tid] = dn[k];
                 if (bad) atomicOr(A.status, bad);
             }
-            // slice partials: <B, D_new> and D_new D_new^T (fixed order over the slice)
-            gacc[tid] = (tid < nsl) ? bd : 0.0;
+            gacc[tid] = bd;
             __syncthreads();
             if (tid == 0) {
                 double s = 0.0;
                 for (int u = 0; u < nsl; ++u) s += gacc[u];
                 A.dpart[c] = s;
             }
-            __syncthreads();
-            if (tid < nsl) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) ring[k * 64 + tid] = dn[k];  // ring idle: slice staging
-            }
-            __syncthreads();
-            for (int o = tid; o < KK; o += NTHREADS) {
-                const int a = o / K, b = o - (o / K) * K;
-                double s = 0.0;
-                for (int u = 0; u < nsl; ++u) s = fma((double)ring[a * 64 + u], (double)ring[b * 64 + u], s);
-                A.Gpart[(int64_t)c * KK + o] = s;
-            }
         }
-        grid_sync(A.bar, A.bar + 1);
-        // ---- G_new (every CTA, same fixed order), objective (CTA 0), restage D
+        stamp(it, 3);
+        grid_sync(A.bar, epoch);
+        // ---- restage D, G_new from the staged D (fp64, fixed order), objective
+        {
+            using DL = DLayout<K>;
+            constexpr int KD = DL::KD;
+            if (dvec) {
+                const int nq = A.Nk >> 2;
+#pragma unroll 2
+                for (int i = tid; i < K * nq; i += NTHREADS) {
+                    const int k = i / nq, l = 4 * (i - k * nq);
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(A.D) + i);
+                    Ds[DL::index(l + 0, k)] = v.x;
+                    Ds[DL::index(l + 1, k)] = v.y;
+                    Ds[DL::index(l + 2, k)] = v.z;
+                    Ds[DL::index(l + 3, k)] = v.w;
+                }
+            } else {
+#pragma unroll 8
+                for (int i = tid; i < K * A.Nk; i += NTHREADS) {
+                    const int k = i / A.Nk, l = i - k * A.Nk;
+                    Ds[DL::index(l, k)] = __ldcg(A.D + i);
+                }
+            }
+            (void)KD;
+        }
+        __syncthreads();
         {
             constexpr int NQ = NTHREADS / KK > 0 ? NTHREADS / KK : 1;
             if (tid < NQ * KK) {
                 const int o = tid % KK, q = tid / KK;
+                const int a = o / K, b = o - (o / K) * K;
                 double s = 0.0;
-                for (int cc = q; cc < nC; cc += NQ) s += __ldcg(A.Gpart + (int64_t)cc * KK + o);
+                for (int l = q; l < A.Nk; l += NQ)
+                    s = fma((double)Ds[DLayout<K>::index(l, a)], (double)Ds[DLayout<K>::index(l, b)], s);
                 gacc[tid] = s;
             }
             __syncthreads();
@@ -666,10 +816,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 double s = 0.0;
                 for (int q = 0; q < NQ; ++q) s += gacc[q * KK + o];
                 Gnew[o] = s;
+                sh.Gs[o] = (float)s;
             }
             __syncthreads();
         }
-        if (c == 0) {
+        if (c == nC - 1) {
             double v0 = 0.0, v1 = 0.0, v2 = 0.0;
             for (int i = tid; i < nC; i += NTHREADS) {
                 v0 += __ldcg(A.vpart + 2 * i);
@@ -677,9 +828,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
             }
             if (it == 0)
                 for (int i = tid; i < A.nby; i += NTHREADS) v1 += __ldcg(A.ypart + i);
-            const double va = block_sum_d(v0, gacc);
-            const double ysq_new = block_sum_d(v1, gacc);
-            const double bdot = block_sum_d(v2, gacc);
+            const double va = block_sum_all(v0, red);
+            const double ysq_new = block_sum_all(v1, red);
+            const double bdot = block_sum_all(v2, red);
             if (tid == 0) {
                 if (it == 0) {
                     ysq = ysq_new;
@@ -699,8 +850,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
         }
         for (int o = tid; o < KK; o += NTHREADS) Gold[o] = Gnew[o];
         __syncthreads();
-        stage_dg<K, LP, NBUF>(A.D, A.Nk, Gold, Ds, sh);
-        __syncthreads();
+        stamp(it, 4);
     }
     if (c == 0)
         for (int o = tid; o < KK; o += NTHREADS) A.Gd[o] = Gold[o];
@@ -709,32 +859,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
 
 }  // namespace
 
+// Largest LP (lambda pairs per thread) the register budget allows for K.
+// register budget for B columns + row partials; the register file is split over the 4 SM
+// sub-partitions (16K each), so it is set by warps per sub-partition: 2 -> 255, 3 -> 168, 4 -> 128
+constexpr int RB = NTHREADS <= 256 ? 200 : (NTHREADS <= 384 ? 150 : 110);
 constexpr int lp_cap(int K) {
-    // registers per compute thread: 2*K*LP (B columns) + RG*K (row partials) + loads
-    return (160 - RG * K) / (2 * K) < 8 ? (160 - RG * K) / (2 * K) : 8;
+    // registers per compute thread: 2*K*LP (B columns) + RG*KD (row partials) + loads/addresses
+    return (RB - RG * ((K + 1) & ~1)) / (2 * K) < 8 ? (RB - RG * ((K + 1) & ~1)) / (2 * K) : 8;
+}
+
+// dynamic smem bytes of the fused kernels
+inline size_t fused_smem_bytes(int Nkp, int K, int LP, int NBG) {
+    const size_t DS = (size_t)2 * TG * LP;
+    const size_t ring = (size_t)NGRP * NBG * tile_floats_of(Nkp, K);
+    return (std::max(ring, (size_t)(NGRP - 1) * DS) + (size_t)((K + 1) & ~1) * Nkp + SCR) * sizeof(float);
 }
 
 template <int K, int LP, int NB>
 inline cudaError_t fused_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
-                             bool first, unsigned* status, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_nmf_fused<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-        attr = true;
+                             int it, unsigned* status, cudaStream_t s) {
+    static size_t attr = 0;  // dynamic smem the kernel is currently allowed (static + dynamic <= 227 KB)
+    if (attr < p.smem_f) {
+        cudaError_t e = cudaFuncSetAttribute(k_nmf_fused<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p.smem_f);
+        if (e != cudaSuccess) return e;
+        attr = p.smem_f;
     }
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     k_nmf_fused<K, LP, NB><<<p.nblk_f, NTHREADS, p.smem_f, s>>>(w.Yp, Np, g.Nk, p.Nkp, V, D, w.Gd, w.Bpart,
-                                                               w.Hpart, w.vpart, first ? 1 : 0, status);
+                                                               w.Hpart, w.vpart, it, status);
     return cudaGetLastError();
 }
 
 template <int K, int LP, int NB>
 inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D,
                                int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_nmf_persist<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-        attr = true;
+    static size_t attr = 0;
+    if (attr < p.smem_f) {
+        cudaError_t e = cudaFuncSetAttribute(k_nmf_persist<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p.smem_f);
+        if (e != cudaSuccess) return e;
+        attr = p.smem_f;
     }
     PersistArgs A;
     A.Yp = w.Yp;
@@ -749,25 +914,27 @@ inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs&
     A.Hpart = w.Hpart;
     A.vpart = w.vpart;
     A.dpart = w.dpart;
-    A.Gpart = w.Gpart;
     A.ypart = w.ypart;
     A.nby = p.nby;
     A.ysq = w.ysq;
     A.obj = obj;
+    A.trace = w.trace;
+    A.trace_iters = w.trace_iters;
     A.bar = bar;
     A.status = status;
     void* args[] = {&A};
+    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);  // grid-barrier arrival counter
+    if (e != cudaSuccess) return e;
     return cudaLaunchCooperativeKernel((const void*)k_nmf_persist<K, LP, NB>, dim3(p.nblk_f), dim3(NTHREADS), args,
                                        p.smem_f, s);
 }
 
-// (K, LP, NBUF) dispatch to a callable templated on the three
+// (K, LP, NBG) dispatch to a callable templated on the three
 template <int K, int LP, class F>
 inline cudaError_t disp_nb(const NmfPlan& p, F&& f) {
     switch (p.nbuf) {
-        case 4: return f.template operator()<K, LP, 4>();
-        case 6: return f.template operator()<K, LP, 6>();
-        case 8: return f.template operator()<K, LP, 8>();
+        case 2: return f.template operator()<K, LP, 2>();
+        case 3: return f.template operator()<K, LP, 3>();
         default: return cudaErrorInvalidValue;
     }
 }
@@ -789,10 +956,10 @@ inline cudaError_t disp_lp(const NmfPlan& p, F&& f) {
 
 // Per-K entry points, defined in nmf_fused_k<K>.cu (one translation unit per K).
 template <int K>
-cudaError_t fused_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, bool first,
+cudaError_t fused_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                            unsigned* status, cudaStream_t s) {
     return disp_lp<K>(p, [&]<int KK, int LP, int NB>() {
-        return fused_klb<KK, LP, NB>(g, p, w, V, D, first, status, s);
+        return fused_klb<KK, LP, NB>(g, p, w, V, D, it, status, s);
     });
 }
 template <int K>
@@ -804,7 +971,7 @@ cudaError_t persist_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w
 }
 #define HSNCT_FUSED_EXTERN(KV)                                                                                  \
     extern template cudaError_t fused_launch_k<KV>(const Geometry&, const NmfPlan&, const NmfWs&, float*,       \
-                                                   const float*, bool, unsigned*, cudaStream_t);                \
+                                                   const float*, int, unsigned*, cudaStream_t);                 \
     extern template cudaError_t persist_launch_k<KV>(const Geometry&, const NmfPlan&, const NmfWs&, float*,     \
                                                      float*, int, double*, unsigned*, unsigned*, cudaStream_t);
 HSNCT_FUSED_EXTERN(1) HSNCT_FUSED_EXTERN(2) HSNCT_FUSED_EXTERN(3) HSNCT_FUSED_EXTERN(4)

@@ -2,7 +2,7 @@
 #include "nmf_fused.cuh"
 
 namespace hsnct {
-template cudaError_t fused_launch_k<7>(const Geometry&, const NmfPlan&, const NmfWs&, float*, const float*, bool,
+template cudaError_t fused_launch_k<7>(const Geometry&, const NmfPlan&, const NmfWs&, float*, const float*, int,
                                         unsigned*, cudaStream_t);
 template cudaError_t persist_launch_k<7>(const Geometry&, const NmfPlan&, const NmfWs&, float*, float*, int,
                                           double*, unsigned*, unsigned*, cudaStream_t);

@@ -70,6 +70,8 @@ def lib():
             L.hsnct_status_string.restype = ctypes.c_char_p
             L.hsnct_last_error.argtypes = []
             L.hsnct_last_error.restype = ctypes.c_char_p
+            L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
+            L.hsnct_debug_trace.restype = i32
             L.hsnct_abi_version.argtypes = []
             L.hsnct_abi_version.restype = i32
             _lib = L
@@ -230,6 +232,19 @@ class Hsnct:
                                     _ptr(Xh), _ptr(V), _ptr(D), _ptr(ws), ws.numel() * ws.element_size(),
                                     _stream(stream, self.device)))
         return Xh
+
+    def debug_trace(self):
+        """Per-iteration, per-CTA phase stamps of the last persistent decompose (ns), as a
+        uint64 array [iters, n_cta, 5], or None when tracing is off (HSNCT_TRACE=1 at create)."""
+        import numpy as np
+        L = lib()
+        n_out, n_cta = ctypes.c_size_t(0), ctypes.c_int(0)
+        _check(L.hsnct_debug_trace(self._h, None, 0, ctypes.byref(n_out), ctypes.byref(n_cta)))
+        if n_out.value == 0:
+            return None
+        buf = np.zeros(n_out.value, dtype=np.uint64)
+        _check(L.hsnct_debug_trace(self._h, ctypes.c_void_p(buf.ctypes.data), buf.size, None, None))
+        return buf.reshape(-1, n_cta.value, 5)
 
     def sync(self, stream=None):
         """Wait for the stream; raise the deferred data/numeric status (hsnct_sync)."""

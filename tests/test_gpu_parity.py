@@ -85,15 +85,38 @@ def test_nmf_deterministic_and_resumable(H):
     h = H(cfg)
     Y = pr["Y"].to(DEV)
     outs = []
-    for split in ((30,), (30,), (11, 19)):
+    # the tile order alternates per iteration within a call, so a
+    # resume after an even number of iterations is bitwise; after an odd number it
+    # differs only by fp32 summation order
+    for split in ((30,), (30,), (12, 18), (11, 19)):
         V = pr["V0"].to(DEV).clone()
         D = pr["D0"].to(DEV).clone()
         for n in split:
             h.subspace_decompose(Y, V, D, n)
         h.sync()
         outs.append((V.cpu(), D.cpu()))
-    for V, D in outs[1:]:
+    for V, D in outs[1:3]:
         assert torch.equal(V, outs[0][0]) and torch.equal(D, outs[0][1])
+    assert rel(outs[3][0], outs[0][0]) < 1e-5 and rel(outs[3][1], outs[0][1]) < 1e-5
+
+
+@pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
+                                        (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
+def test_nmf_per_iteration_fallback(H, monkeypatch, cfg, n_iter):
+    """The per-iteration launch path (used when a cooperative launch is refused)."""
+    monkeypatch.setenv("HSNCT_NO_PERSIST", "1")
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    obj = torch.zeros(2 * n_iter, dtype=torch.float64, device=DEV)
+    l0 = h.kernel_launches
+    h.subspace_decompose(padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4), V, D, n_iter, obj_trace=obj)
+    h.sync()
+    assert h.kernel_launches - l0 >= 2 * n_iter  # really the per-iteration path
+    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter, objective=True)
+    assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
+    np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
 
 
 def test_nmf_fixed_point(H):
