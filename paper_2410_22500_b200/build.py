@@ -18,7 +18,8 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhsnct.so")
 BUILD = os.path.join(HERE, "build")
 
-SOURCES = ["api.cpp", "nmf.cu", "nmf_fused.cu", "fbp.cu", "synth.cu"] + [f"nmf_fused_k{k}.cu" for k in range(1, 9)]
+SOURCES = (["api.cpp", "nmf.cu", "nmf_fused.cu", "nmf_mma.cu", "fbp.cu", "synth.cu"]
+           + [f"nmf_fused_k{k}.cu" for k in range(1, 9)] + [f"nmf_mma_k{k}.cu" for k in range(1, 9)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          f"-I{INC}", f"-I{CSRC}"]
@@ -38,7 +39,12 @@ def _stale(out: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, variant: str = "",
+          defines=()) -> str:
+    """Compile and link libhsnct.so.  A non-empty variant (with extra -D defines) builds an
+    experimental libhsnct_<variant>.so from separate objects (select it with HSNCT_LIB)."""
+    BUILD = os.path.join(HERE, "build" + (f"_{variant}" if variant else ""))
+    LIB = os.path.join(HERE, f"libhsnct_{variant}.so" if variant else "libhsnct.so")
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "hsnct.h"))
@@ -49,7 +55,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         objs.append(o)
         if force or _stale(o, [s, *headers, __file__]):
             extra = ["-Xptxas", "-v"] if ptxas_v and src.endswith(".cu") else []
-            cmds.append([nvcc(), *ARCH, *FLAGS, *extra, "-c", s, "-o", o])
+            cmds.append([nvcc(), *ARCH, *FLAGS, *[f"-D{d}" for d in defines], *extra, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -69,4 +75,6 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv, variant=var, defines=defs))

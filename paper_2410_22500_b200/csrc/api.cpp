@@ -146,6 +146,18 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
     w.trace_iters = h->trace_iters;
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
+    if (h->nmf.mma) {
+        const int nbx = (h->g.Nk + 31) / 32;
+        cudaError_t e = nmf_mma_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1, h->t.status, s);
+        if (e == cudaSuccess) {
+            h->launches += 1;
+            return HSNCT_OK;
+        }
+        // cooperative launch refused: redo the input preparation for the FFMA path below
+        (void)cudaGetLastError();
+        CK(nmf_yplus_launch(h->g, h->nmf, w, Y, ld, h->t.status, s), "decompose init (fallback)");
+        h->launches += 1;
+    }
     if (h->nmf.persist) {
         const int nbx = (h->g.Nk + 31) / 32;
         cudaError_t e = nmf_persist_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1,

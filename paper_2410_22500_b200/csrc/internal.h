@@ -52,6 +52,12 @@ struct NmfPlan {
     int fthreads;    // threads per CTA
     int nblk_f;      // CTAs (persistent, static tile schedule)
     size_t smem_f;   // dynamic smem (tile ring)
+    // tensor-core path (nmf_mma.cuh), K <= 8, persistent only
+    bool mma;
+    int N16;         // Nk rounded up to 16
+    int spw;         // k-steps per warp
+    int nslot;       // tile slots
+    size_t smem_m;   // dynamic smem
     // two-pass fallback (nmf.cu)
     int nblk_v, nchunk, bthreads, nlam_blk;
     int64_t rows_per_chunk;
@@ -94,6 +100,12 @@ cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs&
                                double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                              unsigned* status, cudaStream_t s);
+// tensor-core path: plan, Y+ hi/lo split, all iterations in one cooperative launch
+bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p);
+cudaError_t nmf_ysplit_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                              unsigned* status, cudaStream_t s);
+cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
+                           double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
 // counter words needed by the handle: 1 + ceil(Nk / 32)
 

@@ -522,6 +522,15 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.fused = nmf_fused_plan(g, num_sms, &p);
     const char* np_env = getenv("HSNCT_NO_PERSIST");
     p.persist = p.fused && !(np_env && np_env[0] == '1');
+    // the tensor-core path is persistent-only; its grid equals the fused path's
+    NmfPlan q = p;
+    p.mma = p.persist && nmf_mma_plan(g, num_sms, &q);
+    if (p.mma) {
+        p.N16 = q.N16;
+        p.spw = q.spw;
+        p.nslot = q.nslot;
+        p.smem_m = q.smem_m;
+    }
     // two-pass fallback (K > 8 or very long spectra)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
@@ -551,11 +560,12 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     b += align256((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));   // Gpart
     b += align256(sizeof(double));                                    // ysq
     b += align256((size_t)p.PH * KK * sizeof(double));                // Hpart
-    b += align256((size_t)p.P * g.K * p.Nkp * sizeof(float));         // Bpart
+    const size_t bstride = std::max<size_t>(p.Nkp, p.mma ? p.N16 : 0);
+    b += align256((size_t)p.P * g.K * bstride * sizeof(float));       // Bpart
     b += align256((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));   // L2B
     b += align256((size_t)p.nbx * DG2 * KK * sizeof(double));         // L2H
     if (p.fused) {
-        b += align256((size_t)Np_(g) * p.Nkp * sizeof(float));        // Yp
+        b += align256((size_t)Np_(g) * bstride * sizeof(float));      // Yp (fp32) or Y+ hi/lo halves
         b += align256((size_t)p.nby * sizeof(double));                // ypart
     }
     return b;
@@ -576,11 +586,12 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
     w.Gpart = (double*)take((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));
     w.ysq = (double*)take(sizeof(double));
     w.Hpart = (double*)take((size_t)p.PH * KK * sizeof(double));
-    w.Bpart = (float*)take((size_t)p.P * g.K * p.Nkp * sizeof(float));
+    const size_t bstride = std::max<size_t>(p.Nkp, p.mma ? p.N16 : 0);
+    w.Bpart = (float*)take((size_t)p.P * g.K * bstride * sizeof(float));
     w.L2B = (double*)take((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));
     w.L2H = (double*)take((size_t)p.nbx * DG2 * KK * sizeof(double));
     if (p.fused) {
-        w.Yp = (float*)take((size_t)Np_(g) * p.Nkp * sizeof(float));
+        w.Yp = (float*)take((size_t)Np_(g) * bstride * sizeof(float));
         w.ypart = (double*)take((size_t)p.nby * sizeof(double));
     }
     return w;
@@ -590,7 +601,10 @@ int nmf_init_launches(const NmfPlan& p) { return p.fused ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s) {
-    if (p.fused) {
+    if (p.mma) {
+        cudaError_t e = nmf_ysplit_launch(g, p, w, Y, ld_y, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.fused) {
         cudaError_t e = nmf_yplus_launch(g, p, w, Y, ld_y, status, s);
         if (e != cudaSuccess) return e;
     }

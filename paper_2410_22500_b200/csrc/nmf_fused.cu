@@ -6,7 +6,7 @@ namespace hsnct {
 // Ring slots per compute group: 3 when they fit the shared-memory budget, else 2.
 static int nbuf_for(int Nkp, int LP, int K) {
     for (int nb = 3; nb >= 2; --nb)
-        if (fused_smem_bytes(Nkp, K, LP, nb) <= 212 * 1024) return nb;
+        if (fused_smem_bytes(Nkp, K, LP, nb) <= 208 * 1024) return nb;
     return 0;
 }
 

@@ -31,6 +31,7 @@
 #include <algorithm>
 
 #include "internal.h"
+#include "nmf_common.cuh"
 
 namespace hsnct {
 namespace {
@@ -49,45 +50,6 @@ constexpr int NTHREADS = NGRP * TG;
 constexpr int VWARP = GW - 1;      // warp of a group that stores V (fewest lambda pairs)
 constexpr int HWARP = GW - 2;      // warp of a group that accumulates H
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-// Orders this thread's (and, after a barrier, the CTA's) generic-proxy shared-memory
-// accesses before its subsequent bulk copies into the same buffers.
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-// Generic -> async proxy ordering for global memory (V rows written by one
-// iteration are read by the next iteration's bulk copies).
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 // d = a * b + c on both halves (one packed FFMA2 on sm_100a), each half rounded
 // exactly like fmaf.
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
@@ -101,26 +63,6 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
         : "=f"(d.x), "=f"(d.y)
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
     return d;
-}
-
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Fixed-order block reduction of one double per thread (result valid in thread 0).
-__device__ __forceinline__ double block_sum_d(double v, double* sh) {
-    v = warp_sum_d(v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
-    __syncthreads();
-    return s;
 }
 
 // Warp transpose-reduce of N values per lane.  On return the lane holds
@@ -605,25 +547,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
     }
 }
 
-// Grid barrier for a cooperative launch (all CTAs co-resident): a monotone arrival
-// counter (zeroed by the host before the launch); barrier number e completes when the
-// counter reaches e * nCTA.  One release-add per CTA, acquire polling, no second atomic.
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned& epoch) {
-    __syncthreads();
-    ++epoch;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(count) : "memory");
-        const unsigned target = epoch * gridDim.x;
-        unsigned cur;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(count) : "memory");
-        } while ((int)(cur - target) < 0);
-        __threadfence();
-    }
-    __syncthreads();
-}
-
 struct PersistArgs {
     const float* Yp;
     int64_t Np;
@@ -635,6 +558,7 @@ struct PersistArgs {
     double* Hpart;   // [nCTA][KK]
     double* vpart;   // [nCTA][2]
     double* dpart;   // [nCTA]
+    double* Gpart;   // [nCTA][KK] slice partials of D_new D_new^T
     const double* ypart;
     int nby;
     double* ysq;
@@ -644,19 +568,6 @@ struct PersistArgs {
     unsigned* bar;   // arrival counter, zero at launch
     unsigned* status;
 };
-
-// Fixed-order block reduction of one double per thread, result in every thread.
-__device__ __forceinline__ double block_sum_all(double v, double* sh) {
-    v = warp_sum_d(v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[warp] = v;
-    __syncthreads();
-    double s = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
-    __syncthreads();
-    return s;
-}
 
 // All n_iter Lee-Seung iterations in one cooperative launch.  Per iteration:
 //   pass (the next pass's head tiles are issued as soon as it ends) -> grid barrier
@@ -673,6 +584,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
     __shared__ double Hs[KK], Gold[KK], Gnew[KK];
     __shared__ double gacc[NTHREADS];
     __shared__ double red[NTHREADS / 32];
+    __shared__ double dnew[K * 64];   // the CTA's lambda slice of D_new (nsl <= 64)
     extern __shared__ __align__(128) float smem[];
     const int tid = threadIdx.x;
     const int nC = gridDim.x, c = blockIdx.x;
@@ -724,14 +636,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 double s = 0.0;
                 if (o < KK) {
                     const double* src = A.Hpart + o;
-#pragma unroll 8
-                    for (int cc = q; cc < nC; cc += NQ) s += __ldcg(src + (int64_t)cc * KK);
+                    s = batched_sum(q, NQ, nC, [&](int cc) { return __ldcg(src + (int64_t)cc * KK); });
                 } else {
                     const int ob = o - KK, k = ob / nsl, l = l0 + (ob - (ob / nsl) * nsl);
                     const float* src = A.Bpart + (int64_t)k * A.Nkp + l;
                     const int64_t stride = (int64_t)K * A.Nkp;
-#pragma unroll 8
-                    for (int cc = q; cc < nC; cc += NQ) s += (double)__ldcg(src + (int64_t)cc * stride);
+                    s = batched_sum(q, NQ, nC, [&](int cc) { return (double)__ldcg(src + (int64_t)cc * stride); });
                 }
                 gacc[tid] = s;
             }
@@ -752,7 +662,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 unsigned bad = 0;
                 double d[K];
 #pragma unroll
-                for (int k = 0; k < K; ++k) d[k] = (double)__ldcg(A.D + (int64_t)k * A.Nk + l);
+                for (int k = 0; k < K; ++k) d[k] = (double)Ds[DLayout<K>::index(l, k)];  // = D_old
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     double hd = 0.0;
@@ -763,6 +673,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                     if (!isfinite(dn)) bad |= ST_NUMERIC;
                     bd += B * (double)dn;
                     A.D[(int64_t)k * A.Nk + l] = dn;
+                    dnew[k * 64 + tid] = (double)dn;
                 }
                 if (bad) atomicOr(A.status, bad);
             }
@@ -773,16 +684,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 for (int u = 0; u < nsl; ++u) s += gacc[u];
                 A.dpart[c] = s;
             }
+            // slice partial of G_new = D_new D_new^T (fixed order over the slice)
+            for (int o = tid; o < KK; o += NTHREADS) {
+                const int a = o / K, b = o - (o / K) * K;
+                double s = 0.0;
+                for (int u = 0; u < nsl; ++u) s = fma(dnew[a * 64 + u], dnew[b * 64 + u], s);
+                A.Gpart[(int64_t)c * KK + o] = s;
+            }
         }
         stamp(it, 3);
         grid_sync(A.bar, epoch);
-        // ---- restage D, G_new from the staged D (fp64, fixed order), objective
+        // ---- G_new from the slice partials (every CTA, same fixed order; its loads are
+        //      issued together with the D restage), objective (last CTA)
         {
+            constexpr int NQ = NTHREADS / KK > 0 ? NTHREADS / KK : 1;
+            double s = 0.0;
+            if (tid < NQ * KK) {
+                const int o = tid % KK, q = tid / KK;
+                s = batched_sum(q, NQ, nC, [&](int cc) { return __ldcg(A.Gpart + (int64_t)cc * KK + o); });
+            }
             using DL = DLayout<K>;
-            constexpr int KD = DL::KD;
             if (dvec) {
                 const int nq = A.Nk >> 2;
-#pragma unroll 2
+#pragma unroll 8
                 for (int i = tid; i < K * nq; i += NTHREADS) {
                     const int k = i / nq, l = 4 * (i - k * nq);
                     const float4 v = __ldcg(reinterpret_cast<const float4*>(A.D) + i);
@@ -798,25 +722,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                     Ds[DL::index(l, k)] = __ldcg(A.D + i);
                 }
             }
-            (void)KD;
-        }
-        __syncthreads();
-        {
-            constexpr int NQ = NTHREADS / KK > 0 ? NTHREADS / KK : 1;
-            if (tid < NQ * KK) {
-                const int o = tid % KK, q = tid / KK;
-                const int a = o / K, b = o - (o / K) * K;
-                double s = 0.0;
-                for (int l = q; l < A.Nk; l += NQ)
-                    s = fma((double)Ds[DLayout<K>::index(l, a)], (double)Ds[DLayout<K>::index(l, b)], s);
-                gacc[tid] = s;
-            }
+            if (tid < NQ * KK) gacc[tid] = s;
             __syncthreads();
             for (int o = tid; o < KK; o += NTHREADS) {
-                double s = 0.0;
-                for (int q = 0; q < NQ; ++q) s += gacc[q * KK + o];
-                Gnew[o] = s;
-                sh.Gs[o] = (float)s;
+                double t = 0.0;
+                for (int q = 0; q < NQ; ++q) t += gacc[q * KK + o];
+                Gnew[o] = t;
+                sh.Gs[o] = (float)t;
             }
             __syncthreads();
         }
@@ -914,6 +826,7 @@ inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs&
     A.Hpart = w.Hpart;
     A.vpart = w.vpart;
     A.dpart = w.dpart;
+    A.Gpart = w.Gpart;
     A.ypart = w.ypart;
     A.nby = p.nby;
     A.ysq = w.ysq;

@@ -1,0 +1,7 @@
+// Instantiation of the tensor-core NMF kernel for K = 3 (see nmf_mma.cuh).
+#include "nmf_mma.cuh"
+
+namespace hsnct {
+template cudaError_t mma_launch_k<3>(const Geometry&, const NmfPlan&, const NmfWs&, float*, float*, int, double*,
+                                      unsigned*, unsigned*, cudaStream_t);
+}  // namespace hsnct

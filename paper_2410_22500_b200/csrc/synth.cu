@@ -12,6 +12,20 @@ namespace hsnct {
 namespace {
 
 constexpr int ST = 256;
+
+// (x, x) * b + c on both halves: one packed FFMA2 with a broadcast scalar
+__device__ __forceinline__ float2 ffma2s(float x, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %2};\n\t"
+        "mov.b64 rb, {%3, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(x), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
 constexpr int BCH = 512;   // max bins per block column (D window in smem <= K * 512 floats)
 
 template <int K, bool VEC>
@@ -57,6 +71,64 @@ __global__ void __launch_bounds__(ST) k_synth(const float* __restrict__ X, const
     }
 }
 
+// Vectorised variant (Xh 16-byte aligned, ld % 4 == 0): a warp owns 32 consecutive bin
+// quads (128 bins) of a bin group and walks chunks of 32 consecutive voxels: X[k][chunk] is
+// one coalesced load per k, broadcast voxel by voxel with a shuffle; each lane keeps its D
+// quads in registers; packed f32x2 FMAs; one streaming 16-byte store per lane per voxel.
+// Grid: (voxel-chunk blocks, bin groups).
+template <int K>
+__global__ void __launch_bounds__(ST) k_synth_v(const float* __restrict__ X, const float* __restrict__ D, int64_t Nx,
+                                                int Nk, int64_t n0, int64_t nn, int b0, int nb,
+                                                float* __restrict__ Xh, int64_t ld) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = blockIdx.y * 32 + lane;  // bin quad of this lane
+    const int nq = (nb + 3) >> 2;
+    const bool act = q < nq;
+    float4 d[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int b = 4 * q + e;
+            v[e] = (act && b < nb) ? __ldg(D + (int64_t)k * Nk + b0 + b) : 0.f;
+        }
+        d[k] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    const bool full = 4 * q + 3 < nb;
+    const int64_t nchunk = (nn + 31) >> 5;
+    const int64_t wstride = (int64_t)gridDim.x * (ST / 32);
+    for (int64_t ch = (int64_t)blockIdx.x * (ST / 32) + warp; ch < nchunk; ch += wstride) {
+        const int64_t nb0 = ch << 5;
+        const int cnt = (int)min((int64_t)32, nn - nb0);
+        float xk[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) xk[k] = lane < cnt ? __ldg(X + (int64_t)k * Nx + n0 + nb0 + lane) : 0.f;
+        float* dst = Xh + nb0 * ld + 4 * q;
+#pragma unroll 4
+        for (int i = 0; i < cnt; ++i) {
+            float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const float x = __shfl_sync(0xffffffffu, xk[k], i);
+                o01 = ffma2s(x, make_float2(d[k].x, d[k].y), o01);
+                o23 = ffma2s(x, make_float2(d[k].z, d[k].w), o23);
+            }
+            if (act) {
+                if (full) {
+                    __stcs(reinterpret_cast<float4*>(dst), make_float4(o01.x, o01.y, o23.x, o23.y));
+                } else {
+                    const int valid = nb - 4 * q;
+                    __stcs(dst, o01.x);
+                    if (valid > 1) __stcs(dst + 1, o01.y);
+                    if (valid > 2) __stcs(dst + 2, o23.x);
+                }
+            }
+            dst += ld;
+        }
+    }
+}
+
 #define HSNCT_K_CASES(M) \
     M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
 
@@ -73,6 +145,14 @@ cudaError_t synth_k(const Geometry& g, const float* X, const float* D, int s0, i
     const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(want, (per_col + ST - 1) / ST));
     dim3 grid(nblk, ncol);
     const bool vec = ((reinterpret_cast<uintptr_t>(Xh) & 15) == 0) && (ld % 4 == 0);
+    if (vec) {
+        const int nqg = (nb + 127) / 128;
+        const int64_t wblocks = ((nn + 31) / 32 + (ST / 32) - 1) / (ST / 32);
+        const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 8) / nqg);
+        dim3 gv((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, wblocks)), nqg);
+        k_synth_v<K><<<gv, ST, 0, s>>>(X, D, Nx, g.Nk, n0, nn, b0, nb, Xh, ld);
+        return cudaGetLastError();
+    }
     if (vec)
         k_synth<K, true><<<grid, ST, 0, s>>>(X, D, Nx, g.Nk, n0, nn, b0, nb, bcw, Xh, ld);
     else

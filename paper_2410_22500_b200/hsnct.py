@@ -14,7 +14,8 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhsnct.so")
+# HSNCT_LIB selects an experimental build variant (paper_2410_22500_b200/build.py --variant=...)
+LIB_PATH = os.environ.get("HSNCT_LIB") or os.path.join(_HERE, "libhsnct.so")
 
 OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
 OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST = range(4)

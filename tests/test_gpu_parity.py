@@ -102,6 +102,23 @@ def test_nmf_deterministic_and_resumable(H):
 
 @pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
                                         (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
+def test_nmf_mma_path(H, monkeypatch, cfg, n_iter):
+    """The opt-in tensor-core (mma.sync, fp16 hi/lo split) persistent kernel."""
+    monkeypatch.setenv("HSNCT_MMA", "1")
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    obj = torch.zeros(2 * n_iter, dtype=torch.float64, device=DEV)
+    h.subspace_decompose(padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4), V, D, n_iter, obj_trace=obj)
+    h.sync()
+    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter, objective=True)
+    assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
+    np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
+
+
+@pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
+                                        (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
 def test_nmf_per_iteration_fallback(H, monkeypatch, cfg, n_iter):
     """The per-iteration launch path (used when a cooperative launch is refused)."""
     monkeypatch.setenv("HSNCT_NO_PERSIST", "1")
