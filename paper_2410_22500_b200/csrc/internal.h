@@ -47,6 +47,7 @@ struct NmfPlan {
     bool persist;    // run all iterations in one cooperative launch (fused path)
     int LP;          // lambda pairs per thread
     int nbuf;        // ring slots per compute group
+    int ngrp;        // compute groups of 4 warps (3 or 4)
     int PB;          // B partials of the fused kernel (2 per CTA)
     int nby;         // blocks of the Y+ preparation kernel
     int fthreads;    // threads per CTA

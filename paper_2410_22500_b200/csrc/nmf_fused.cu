@@ -1,12 +1,14 @@
 // Host side of the fused NMF path: plan, Y+ preparation launch, per-K dispatch.
 #include "nmf_fused.cuh"
 
+#include <cstdlib>
+
 namespace hsnct {
 
 // Ring slots per compute group: 3 when they fit the shared-memory budget, else 2.
-static int nbuf_for(int Nkp, int LP, int K) {
+static int nbuf_for(int Nkp, int LP, int K, int ngrp) {
     for (int nb = 3; nb >= 2; --nb)
-        if (fused_smem_bytes(Nkp, K, LP, nb) <= 208 * 1024) return nb;
+        if (fused_smem_bytes(Nkp, K, LP, nb, ngrp) <= 208 * 1024) return nb;
     return 0;
 }
 
@@ -16,12 +18,17 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int pairs = (g.Nk + 1) / 2;
     const int LP = (pairs + TG - 1) / TG;
     if (LP > lp_cap(g.K)) return false;
-    const int nbuf = nbuf_for(Nkp, LP, g.K);
+    // four groups (more tiles in flight) when the registers and two slots per group fit
+    int ngrp = fits4(g.K, LP) && nbuf_for(Nkp, LP, g.K, 4) >= 2 ? 4 : 3;
+    const char* ng = getenv("HSNCT_NGRP");
+    if (ng && ng[0] == '3') ngrp = 3;
+    const int nbuf = nbuf_for(Nkp, LP, g.K, ngrp);
     if (nbuf < 2) return false;
     p->LP = LP;
     p->nbuf = nbuf;
-    p->fthreads = NTHREADS;
-    p->smem_f = fused_smem_bytes(Nkp, g.K, LP, nbuf);
+    p->ngrp = ngrp;
+    p->fthreads = ngrp * TG;
+    p->smem_f = fused_smem_bytes(Nkp, g.K, LP, nbuf, ngrp);
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const int64_t ntiles = (Np + RG - 1) / RG;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));

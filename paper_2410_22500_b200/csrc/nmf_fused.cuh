@@ -37,16 +37,9 @@ namespace hsnct {
 namespace {
 
 constexpr int RG = 4;              // rows per tile
-#ifndef HSNCT_NGRP
-#define HSNCT_NGRP 3
-#endif
-#ifndef HSNCT_GW
-#define HSNCT_GW 4
-#endif
-constexpr int NGRP = HSNCT_NGRP;   // compute groups
-constexpr int GW = HSNCT_GW;       // warps per group
+constexpr int GW = 4;              // warps per group
 constexpr int TG = GW * 32;        // threads per group
-constexpr int NTHREADS = NGRP * TG;
+constexpr int NTHREADS = 3 * TG;   // default CTA size (3 groups); 4 groups when registers allow
 constexpr int VWARP = GW - 1;      // warp of a group that stores V (fewest lambda pairs)
 constexpr int HWARP = GW - 2;      // warp of a group that accumulates H
 
@@ -159,7 +152,7 @@ __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int6
     }
 }
 
-template <int K, int NBG>
+template <int K, int NBG, int NGRP>
 struct FusedShared {
     static constexpr int GK = RG * K;
     static constexpr int KP = (K + 3) & ~3;
@@ -203,13 +196,14 @@ struct DLayout {
     }
 };
 
-template <int K, int LP, int NBG>
+template <int K, int LP, int NBG, int NGRP>
 struct Pass {
     static constexpr int GK = RG * K;
     static constexpr int KP = (K + 3) & ~3;
     static constexpr int KK = K * K;
     static constexpr int DS = 2 * TG * LP;
-    using Sh = FusedShared<K, NBG>;
+    using Sh = FusedShared<K, NBG, NGRP>;
+    static constexpr int NTH = NGRP * TG;
 
     const float* __restrict__ Yp;
     int64_t Np;
@@ -464,7 +458,7 @@ struct Pass {
             }
             __syncthreads();
         }
-        for (int o = tid; o < KK; o += NTHREADS) {
+        for (int o = tid; o < KK; o += NTH) {
             double h = sh.hs[0][o];
             for (int gg = 1; gg < NGRP; ++gg) h += sh.hs[gg][o];
             Hout[o] = h;
@@ -485,9 +479,9 @@ struct Pass {
 };
 
 // Shared prologue: mbarriers, release counters, zeroed ring + slack.
-template <int K, int NBG>
-__device__ __forceinline__ void fused_prologue(FusedShared<K, NBG>& sh, float* ring, size_t ring_floats) {
-    for (size_t i = threadIdx.x; i < ring_floats; i += NTHREADS) ring[i] = 0.f;
+template <int K, int NBG, int NGRP>
+__device__ __forceinline__ void fused_prologue(FusedShared<K, NBG, NGRP>& sh, float* ring, size_t ring_floats) {
+    for (size_t i = threadIdx.x; i < ring_floats; i += blockDim.x) ring[i] = 0.f;
     if (threadIdx.x == 0) {
         for (int g = 0; g < NGRP; ++g)
             for (int b = 0; b < NBG; ++b) {
@@ -508,16 +502,16 @@ __device__ __forceinline__ void stage_dg(const float* __restrict__ D, int Nk, in
     using DL = DLayout<K>;
     constexpr int KD = DL::KD;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < KD * Nkp; i += NTHREADS) {
+    for (int i = threadIdx.x; i < KD * Nkp; i += blockDim.x) {
         const int k = i / Nkp, l = i - k * Nkp;
         Ds[DL::index(l, k)] = (k < K && l < Nk) ? __ldcg(D + (int64_t)k * Nk + l) : 0.f;
     }
-    for (int i = threadIdx.x; i < K * K; i += NTHREADS) Gs[i] = (float)Gsrc[i];
+    for (int i = threadIdx.x; i < K * K; i += blockDim.x) Gs[i] = (float)Gsrc[i];
 }
 
 // One iteration's row pass per launch (fallback when a cooperative launch is refused).
-template <int K, int LP, int NBG>
-__global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restrict__ Yp, int64_t Np, int Nk,
+template <int K, int LP, int NBG, int NGRP>
+__global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_fused(const float* __restrict__ Yp, int64_t Np, int Nk,
                                                            int Nkp, float* __restrict__ V,
                                                            const float* __restrict__ D,
                                                            const double* __restrict__ Gd,
@@ -525,15 +519,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_fused(const float* __restri
                                                            double* __restrict__ Hpart,
                                                            double* __restrict__ vpart, int it,
                                                            unsigned* __restrict__ status) {
-    using P = Pass<K, LP, NBG>;
+    using P = Pass<K, LP, NBG, NGRP>;
     constexpr int DS = P::DS;
-    __shared__ FusedShared<K, NBG> sh;
+    __shared__ FusedShared<K, NBG, NGRP> sh;
     extern __shared__ __align__(128) float smem[];
     const size_t tf = tile_floats_of(Nkp, K);
     const size_t ring_floats = (size_t)NGRP * NBG * tf;
     float* ring = smem;
     float* Ds = smem + max(ring_floats, (size_t)(NGRP - 1) * DS);  // the ring doubles as the B-combine scratch
-    fused_prologue<K, NBG>(sh, ring, ring_floats);
+    fused_prologue<K, NBG, NGRP>(sh, ring, ring_floats);
     stage_dg<K>(D, Nk, Nkp, Gd, Ds, sh.Gs);
     __syncthreads();
     const int64_t ntiles = (Np + RG - 1) / RG;
@@ -575,15 +569,16 @@ struct PersistArgs {
 //   order (one sweep of loads), D update of the slice, <B, D_new> slice partial ->
 //   grid barrier -> D restaged, G_new = D_new D_new^T from the staged D (every CTA,
 //   same fixed order, fp64), objective (last CTA, which has the fewest tiles).
-template <int K, int LP, int NBG>
-__global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
-    using P = Pass<K, LP, NBG>;
+template <int K, int LP, int NBG, int NGRP>
+__global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
+    using P = Pass<K, LP, NBG, NGRP>;
+    constexpr int NTH = NGRP * TG;
     constexpr int DS = P::DS;
     constexpr int KK = K * K;
-    __shared__ FusedShared<K, NBG> sh;
+    __shared__ FusedShared<K, NBG, NGRP> sh;
     __shared__ double Hs[KK], Gold[KK], Gnew[KK];
-    __shared__ double gacc[NTHREADS];
-    __shared__ double red[NTHREADS / 32];
+    __shared__ double gacc[NTH];
+    __shared__ double red[NTH / 32];
     __shared__ double dnew[K * 64];   // the CTA's lambda slice of D_new (nsl <= 64)
     extern __shared__ __align__(128) float smem[];
     const int tid = threadIdx.x;
@@ -593,8 +588,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
     float* ring = smem;
     float* Ds = smem + max(ring_floats, (size_t)(NGRP - 1) * DS);  // the ring doubles as the B-combine scratch
     double* Bsl = reinterpret_cast<double*>(Ds + (size_t)DLayout<K>::KD * A.Nkp);  // [SCR/2] B slice (fp64)
-    fused_prologue<K, NBG>(sh, ring, ring_floats);
-    for (int i = tid; i < KK; i += NTHREADS) Gold[i] = A.Gd[i];
+    fused_prologue<K, NBG, NGRP>(sh, ring, ring_floats);
+    for (int i = tid; i < KK; i += NTH) Gold[i] = A.Gd[i];
     __syncthreads();
     stage_dg<K>(A.D, A.Nk, A.Nkp, Gold, Ds, sh.Gs);
     __syncthreads();
@@ -630,7 +625,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
         // ---- H (KK outputs) and the B slice (K x nsl outputs) over the nC partials
         {
             const int nB = K * nsl, nout = KK + nB;
-            const int NQ = max(1, NTHREADS / nout);
+            const int NQ = max(1, NTH / nout);
             if (tid < NQ * nout) {
                 const int o = tid % nout, q = tid / nout;
                 double s = 0.0;
@@ -646,7 +641,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 gacc[tid] = s;
             }
             __syncthreads();
-            for (int o = tid; o < nout; o += NTHREADS) {
+            for (int o = tid; o < nout; o += NTH) {
                 double s = 0.0;
                 for (int q = 0; q < NQ; ++q) s += gacc[q * nout + o];
                 if (o < KK) Hs[o] = s;
@@ -685,7 +680,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 A.dpart[c] = s;
             }
             // slice partial of G_new = D_new D_new^T (fixed order over the slice)
-            for (int o = tid; o < KK; o += NTHREADS) {
+            for (int o = tid; o < KK; o += NTH) {
                 const int a = o / K, b = o - (o / K) * K;
                 double s = 0.0;
                 for (int u = 0; u < nsl; ++u) s = fma(dnew[a * 64 + u], dnew[b * 64 + u], s);
@@ -697,7 +692,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
         // ---- G_new from the slice partials (every CTA, same fixed order; its loads are
         //      issued together with the D restage), objective (last CTA)
         {
-            constexpr int NQ = NTHREADS / KK > 0 ? NTHREADS / KK : 1;
+            constexpr int NQ = NTH / KK > 0 ? NTH / KK : 1;
             double s = 0.0;
             if (tid < NQ * KK) {
                 const int o = tid % KK, q = tid / KK;
@@ -707,7 +702,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
             if (dvec) {
                 const int nq = A.Nk >> 2;
 #pragma unroll 8
-                for (int i = tid; i < K * nq; i += NTHREADS) {
+                for (int i = tid; i < K * nq; i += NTH) {
                     const int k = i / nq, l = 4 * (i - k * nq);
                     const float4 v = __ldcg(reinterpret_cast<const float4*>(A.D) + i);
                     Ds[DL::index(l + 0, k)] = v.x;
@@ -717,14 +712,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 }
             } else {
 #pragma unroll 8
-                for (int i = tid; i < K * A.Nk; i += NTHREADS) {
+                for (int i = tid; i < K * A.Nk; i += NTH) {
                     const int k = i / A.Nk, l = i - k * A.Nk;
                     Ds[DL::index(l, k)] = __ldcg(A.D + i);
                 }
             }
             if (tid < NQ * KK) gacc[tid] = s;
             __syncthreads();
-            for (int o = tid; o < KK; o += NTHREADS) {
+            for (int o = tid; o < KK; o += NTH) {
                 double t = 0.0;
                 for (int q = 0; q < NQ; ++q) t += gacc[q * KK + o];
                 Gnew[o] = t;
@@ -732,14 +727,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
             }
             __syncthreads();
         }
-        if (c == nC - 1) {
+        if (c == nC - 1 && (A.obj || it == 0)) {  // the objective trace (and the Y+ = 0 check)
             double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-            for (int i = tid; i < nC; i += NTHREADS) {
+            for (int i = tid; i < nC; i += NTH) {
                 v0 += __ldcg(A.vpart + 2 * i);
                 v2 += __ldcg(A.dpart + i);
             }
             if (it == 0)
-                for (int i = tid; i < A.nby; i += NTHREADS) v1 += __ldcg(A.ypart + i);
+                for (int i = tid; i < A.nby; i += NTH) v1 += __ldcg(A.ypart + i);
             const double va = block_sum_all(v0, red);
             const double ysq_new = block_sum_all(v1, red);
             const double bdot = block_sum_all(v2, red);
@@ -760,56 +755,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_nmf_persist(PersistArgs A) {
                 }
             }
         }
-        for (int o = tid; o < KK; o += NTHREADS) Gold[o] = Gnew[o];
+        for (int o = tid; o < KK; o += NTH) Gold[o] = Gnew[o];
         __syncthreads();
         stamp(it, 4);
     }
     if (c == 0)
-        for (int o = tid; o < KK; o += NTHREADS) A.Gd[o] = Gold[o];
+        for (int o = tid; o < KK; o += NTH) A.Gd[o] = Gold[o];
     if (tid == 0 && sh.bad) atomicOr(A.status, sh.bad);
 }
 
 }  // namespace
 
 // Largest LP (lambda pairs per thread) the register budget allows for K.
-// register budget for B columns + row partials; the register file is split over the 4 SM
-// sub-partitions (16K each), so it is set by warps per sub-partition: 2 -> 255, 3 -> 168, 4 -> 128
-constexpr int RB = NTHREADS <= 256 ? 200 : (NTHREADS <= 384 ? 150 : 110);
+// The register file is split over the 4 SM sub-partitions (16K each), so the budget is set
+// by warps per sub-partition: 3 (12 warps, three groups) -> 168, 4 (16 warps) -> 128.
+// Budget for the B columns (2*K*LP) + row partials (RG*KD), the rest is loads/addresses.
 constexpr int lp_cap(int K) {
-    // registers per compute thread: 2*K*LP (B columns) + RG*KD (row partials) + loads/addresses
-    return (RB - RG * ((K + 1) & ~1)) / (2 * K) < 8 ? (RB - RG * ((K + 1) & ~1)) / (2 * K) : 8;
+    return (150 - RG * ((K + 1) & ~1)) / (2 * K) < 8 ? (150 - RG * ((K + 1) & ~1)) / (2 * K) : 8;
 }
+// four groups (16 warps, 128 registers) when the per-thread state fits
+__host__ __device__ constexpr bool fits4(int K, int LP) { return 2 * K * LP + RG * ((K + 1) & ~1) <= 64; }
 
 // dynamic smem bytes of the fused kernels
-inline size_t fused_smem_bytes(int Nkp, int K, int LP, int NBG) {
+inline size_t fused_smem_bytes(int Nkp, int K, int LP, int NBG, int NGRP) {
     const size_t DS = (size_t)2 * TG * LP;
     const size_t ring = (size_t)NGRP * NBG * tile_floats_of(Nkp, K);
     return (std::max(ring, (size_t)(NGRP - 1) * DS) + (size_t)((K + 1) & ~1) * Nkp + SCR) * sizeof(float);
 }
 
-template <int K, int LP, int NB>
+template <int K, int LP, int NB, int NG>
 inline cudaError_t fused_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
                              int it, unsigned* status, cudaStream_t s) {
     static size_t attr = 0;  // dynamic smem the kernel is currently allowed (static + dynamic <= 227 KB)
     if (attr < p.smem_f) {
-        cudaError_t e = cudaFuncSetAttribute(k_nmf_fused<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_nmf_fused<K, LP, NB, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)p.smem_f);
         if (e != cudaSuccess) return e;
         attr = p.smem_f;
     }
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    k_nmf_fused<K, LP, NB><<<p.nblk_f, NTHREADS, p.smem_f, s>>>(w.Yp, Np, g.Nk, p.Nkp, V, D, w.Gd, w.Bpart,
-                                                               w.Hpart, w.vpart, it, status);
+    k_nmf_fused<K, LP, NB, NG><<<p.nblk_f, NG * TG, p.smem_f, s>>>(w.Yp, Np, g.Nk, p.Nkp, V, D, w.Gd, w.Bpart,
+                                                                  w.Hpart, w.vpart, it, status);
     return cudaGetLastError();
 }
 
-template <int K, int LP, int NB>
+template <int K, int LP, int NB, int NG>
 inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D,
                                int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
     static size_t attr = 0;
     if (attr < p.smem_f) {
-        cudaError_t e = cudaFuncSetAttribute(k_nmf_persist<K, LP, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)p.smem_f);
+        cudaError_t e = cudaFuncSetAttribute(k_nmf_persist<K, LP, NB, NG>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_f);
         if (e != cudaSuccess) return e;
         attr = p.smem_f;
     }
@@ -838,16 +834,20 @@ inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs&
     void* args[] = {&A};
     cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);  // grid-barrier arrival counter
     if (e != cudaSuccess) return e;
-    return cudaLaunchCooperativeKernel((const void*)k_nmf_persist<K, LP, NB>, dim3(p.nblk_f), dim3(NTHREADS), args,
-                                       p.smem_f, s);
+    return cudaLaunchCooperativeKernel((const void*)k_nmf_persist<K, LP, NB, NG>, dim3(p.nblk_f), dim3(NG * TG),
+                                       args, p.smem_f, s);
 }
 
-// (K, LP, NBG) dispatch to a callable templated on the three
+// (K, LP, NBG, NGRP) dispatch to a callable templated on the four
 template <int K, int LP, class F>
 inline cudaError_t disp_nb(const NmfPlan& p, F&& f) {
-    switch (p.nbuf) {
-        case 2: return f.template operator()<K, LP, 2>();
-        case 3: return f.template operator()<K, LP, 3>();
+    constexpr int NG4 = fits4(K, LP) ? 4 : 3;
+    if (p.ngrp == 4 && NG4 != 4) return cudaErrorInvalidValue;
+    switch (p.nbuf * 10 + p.ngrp) {
+        case 23: return f.template operator()<K, LP, 2, 3>();
+        case 33: return f.template operator()<K, LP, 3, 3>();
+        case 24: return f.template operator()<K, LP, 2, NG4>();
+        case 34: return f.template operator()<K, LP, 3, NG4>();
         default: return cudaErrorInvalidValue;
     }
 }
@@ -871,15 +871,15 @@ inline cudaError_t disp_lp(const NmfPlan& p, F&& f) {
 template <int K>
 cudaError_t fused_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                            unsigned* status, cudaStream_t s) {
-    return disp_lp<K>(p, [&]<int KK, int LP, int NB>() {
-        return fused_klb<KK, LP, NB>(g, p, w, V, D, it, status, s);
+    return disp_lp<K>(p, [&]<int KK, int LP, int NB, int NG>() {
+        return fused_klb<KK, LP, NB, NG>(g, p, w, V, D, it, status, s);
     });
 }
 template <int K>
 cudaError_t persist_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
                              double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
-    return disp_lp<K>(p, [&]<int KK, int LP, int NB>() {
-        return persist_klb<KK, LP, NB>(g, p, w, V, D, n_iter, obj, bar, status, s);
+    return disp_lp<K>(p, [&]<int KK, int LP, int NB, int NG>() {
+        return persist_klb<KK, LP, NB, NG>(g, p, w, V, D, n_iter, obj, bar, status, s);
     });
 }
 #define HSNCT_FUSED_EXTERN(KV)                                                                                  \
