@@ -301,8 +301,11 @@ def make_init(Y: torch.Tensor, K: int, seed: int):
     """s = sqrt(mean(Y+)/K); V0 = s (1-U), D0 = s (1-U), U ~ U[0,1): strictly positive (R4)."""
     g = torch.Generator(device=Y.device)
     g.manual_seed(seed)
-    s = math.sqrt(max(float(Y.clamp_min(0).double().mean()), 1e-12) / K)
     Np, Nk = Y.shape
+    tot = 0.0  # mean(Y+) in fp64, accumulated over row chunks (no full-size fp64 copy of Y)
+    for p0 in range(0, Np, 1 << 18):
+        tot += float(Y[p0:p0 + (1 << 18)].clamp_min(0).sum(dtype=torch.float64))
+    s = math.sqrt(max(tot / (Np * Nk), 1e-12) / K)
     V0 = (s * (1.0 - torch.rand((Np, K), generator=g, device=Y.device, dtype=torch.float64))).float()
     D0 = (s * (1.0 - torch.rand((K, Nk), generator=g, device=Y.device, dtype=torch.float64))).float()
     return V0, D0
