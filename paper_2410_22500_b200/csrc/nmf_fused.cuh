@@ -222,10 +222,12 @@ struct Pass {
         const int64_t pos = fwd ? q : (nmine - 1 - q);
         return ((int64_t)blockIdx.x + pos * (int64_t)gridDim.x) * RG;
     }
-    // Issue the group-g tile with running group counter n and sequence index q.
-    __device__ __forceinline__ void issue(int g, int64_t n, int64_t q, bool fwd) const {
-        const int b = (int)(n % NBG);
-        const int64_t r0 = row0(q, fwd);
+    // Row step between consecutive tiles of one group in a pass (direction fwd).
+    __device__ __forceinline__ int64_t rstride(bool fwd) const {
+        return (fwd ? (int64_t)1 : (int64_t)-1) * NGRP * (int64_t)gridDim.x * RG;
+    }
+    // Copy the tile starting at row r0 (4 Y+ rows, then its 4 old V rows) into slot b of group g.
+    __device__ __forceinline__ void issue(int g, int b, int64_t r0) const {
         const int nv = (int)min((int64_t)RG, Np - r0);
         const unsigned bytes = (unsigned)(nv * Nkp * sizeof(float));
         const unsigned vbytes = nv == RG ? (unsigned)(RG * K * sizeof(float)) : 0u;  // 16K bytes
@@ -235,10 +237,16 @@ struct Pass {
         bulk_g2s(slot, Yp + r0 * Nkp, bytes, bar);
         if (vbytes) bulk_g2s(slot + (size_t)RG * Nkp, V + r0 * K, vbytes, bar);
     }
-    // Leader of group g: the first NBG tiles of a pass (counter base n0).
+    // Leader of group g: the first NBG tiles of a pass (running group tile counter n0).
     __device__ __forceinline__ void issue_head(int g, int64_t n0, bool fwd) const {
         const int64_t c = count_g(g);
-        for (int64_t m = 0; m < min((int64_t)NBG, c); ++m) issue(g, n0 + m, g + (int64_t)NGRP * m, fwd);
+        int b = (int)(n0 % NBG);
+        int64_t r0 = row0(g, fwd);
+        for (int64_t m = 0; m < min((int64_t)NBG, c); ++m) {
+            issue(g, b, r0);
+            b = b + 1 == NBG ? 0 : b + 1;
+            r0 += rstride(fwd);
+        }
     }
 
     // One pass over this CTA's tiles with the current D (Ds) and G (sh.Gs).
@@ -271,13 +279,15 @@ struct Pass {
 #pragma unroll
         for (int x = 0; x < (KK + 31) / 32; ++x) hacc[x] = 0.0;
         unsigned bad = 0;
-        for (int64_t m = 0; m < cnt; ++m) {
-            const int64_t n = n0 + m;
-            const int b = (int)(n % NBG);
-            const int64_t q = g + (int64_t)NGRP * m;
-            const int64_t r0 = row0(q, fwd);
+        // running slot / mbarrier phase / first row of the group's current tile (no 64-bit
+        // division or multiply per tile)
+        int b = (int)(n0 % NBG);
+        unsigned ph = (unsigned)((n0 / NBG) & 1);
+        const int64_t rs = rstride(fwd);
+        int64_t r0 = row0(g, fwd);
+        for (int64_t m = 0; m < cnt; ++m, r0 += rs) {
             const int nv = (int)min((int64_t)RG, Np - r0);
-            mbar_wait(&sh.full[g][b], (unsigned)((n / NBG) & 1));
+            mbar_wait(&sh.full[g][b], ph);
             const float* slot = ring + (size_t)(g * NBG + b) * tf;
             const float* yb = slot + 2 * t;
             // ---- V-update factor V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old
@@ -408,9 +418,13 @@ struct Pass {
                 if (atomicAdd(&sh.rel[g][b], 1u) % GW == GW - 1) {
                     if (m + NBG < cnt) {
                         fence_proxy_async();
-                        issue(g, n + NBG, q + (int64_t)NGRP * NBG, fwd);
+                        issue(g, b, r0 + NBG * rs);
                     }
                 }
+            }
+            if (++b == NBG) {
+                b = 0;
+                ph ^= 1u;
             }
         }
         // ---- per-group partials to smem
