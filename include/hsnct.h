@@ -106,8 +106,9 @@ hsnct_status hsnct_create(const hsnct_geom* g, int device, hsnct_t* out);
 void hsnct_destroy(hsnct_t h);
 
 /* Workspace bytes the caller must provide for `op` (hsnct_op).  0 on a bad
- * handle / op.  HSNCT_OP_DHR returns the size for a one-slice window; larger
- * workspaces let hsnct_dhr process more slices per pass. */
+ * handle / op.  HSNCT_OP_DHR returns the size for one slice and all N_k bins
+ * (filtered sinograms); hsnct_dhr accepts any workspace of at least one slice x 16
+ * bins and processes as many (bin chunks x slices) per launch as fit. */
 size_t hsnct_workspace_bytes(hsnct_t h, int op);
 
 /* Subspace extraction, Eq. 4: n_iter Lee-Seung

@@ -86,8 +86,12 @@ int kc_of(int K) { return (K + 3) & ~3; }
 int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
 
 size_t fbp_ws(const Geometry& g) { return a256((size_t)Np_of(g) * kc_of(g.K) * sizeof(float)); }
+// Filtered sinograms of one slice for one chunk of dhr_kc bins.
+size_t dhr_ws_chunk_slice(const Geometry& g) { return (size_t)g.Nv * g.Nc * dhr_kc(g) * sizeof(float); }
+// Workspace for one slice and all N_k bins (hsnct_workspace_bytes(DHR)); a workspace of
+// a single chunk-slice is the minimum.
 size_t dhr_ws_per_slice(const Geometry& g) {
-    return (size_t)g.Nv * g.Nc * dhr_kc(g) * sizeof(float);
+    return dhr_ws_chunk_slice(g) * (size_t)((g.Nk + dhr_kc(g) - 1) / dhr_kc(g));
 }
 int64_t fhr_window_slices(const Geometry& g) {
     const size_t per = (size_t)g.Nc * g.Nc * g.Nk * sizeof(float);
@@ -438,7 +442,7 @@ hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int 
     if ((st = check_y(g, Y, ld_y, "dhr"))) return st;
     if (n_slices == 0 || n_bins == 0) return HSNCT_OK;
     if (!Xh || !aligned(Xh, 4)) return fail(HSNCT_E_ARG, "dhr: Xh is NULL or misaligned");
-    const size_t per = dhr_ws_per_slice(g);
+    const size_t per = dhr_ws_chunk_slice(g);
     if ((st = check_ws(ws, ws_bytes, a256(per), "dhr"))) return st;
     const Range rXh = rng(Xh, ((size_t)(n_slices) * g.Nc * g.Nc - 1) * ld_xh * sizeof(float) + n_bins * sizeof(float));
     if (overlap(rXh, rng(Y, (size_t)Np_of(g) * ld_y * sizeof(float))) || overlap(rXh, rng(ws, ws_bytes)))
@@ -446,10 +450,16 @@ hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int 
     DeviceGuard guard(h->device);
     cudaStream_t s = (cudaStream_t)stream;
     const int kc = dhr_kc(g);
-    const int ns_pass = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_slices, ws_bytes / per));
+    // one ramp + one backprojection launch per pass over (slices x bin chunks) that fits the
+    // workspace: as many bin chunks as possible (the whole window when it fits), then slices
+    const int nchunk_all = (n_bins + kc - 1) / kc;
+    const size_t cap = ws_bytes / per;  // chunk-slices per pass (>= 1)
+    const int chunks_pass = (int)std::min<size_t>((size_t)nchunk_all, cap);
+    const int ns_pass = (int)std::max<size_t>(1, std::min<size_t>((size_t)n_slices, cap / chunks_pass));
     float* Q = static_cast<float*>(ws);
-    for (int b = bin0; b < bin0 + n_bins; b += kc) {
-        const int nch = std::min(kc, bin0 + n_bins - b);
+    for (int c0 = 0; c0 < nchunk_all; c0 += chunks_pass) {
+        const int b = bin0 + c0 * kc;
+        const int nch = std::min(chunks_pass * kc, bin0 + n_bins - b);
         for (int r = slice0; r < slice0 + n_slices; r += ns_pass) {
             const int ns = std::min(ns_pass, slice0 + n_slices - r);
             CK(ramp_filter(g, h->t, Y + b, ld_y, nch, r, ns, Q, kc, s), "dhr ramp filter");

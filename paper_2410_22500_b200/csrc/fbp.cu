@@ -24,27 +24,48 @@ namespace {
 constexpr int RT = 256;      // ramp-filter threads
 constexpr int TILE = 16;     // backprojection voxel tile edge
 constexpr int WMAX = 28;     // detector window per view per tile (>= 16*sqrt(2) + 4)
+// floats per staged detector sample: KC, plus 4 when KC/4 is even (an odd number of
+// 16-byte chunks per sample spreads consecutive samples over all bank groups)
+__host__ __device__ constexpr int bp_pitch(int KC) { return KC + (((KC / 4) % 2 == 0) ? 4 : 0); }
 
 __device__ __forceinline__ unsigned bitrev(unsigned x, int logP) { return __brev(x) >> (32 - logP); }
+
+// (x, x) * b + c on both halves: one packed FFMA2 with a broadcast scalar
+__device__ __forceinline__ float2 ffma2s(float x, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %2};\n\t"
+        "mov.b64 rb, {%3, %4};\n\t"
+        "mov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(x), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
 // One (v, r) detector row-set per block: Nch channels -> npair complex rows of length P.
-__global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64_t ld_in, int Nch,
-                                             int Nv, int Nr, int Nc, int P, int logP, int s0,
+__global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64_t ld_in, int NchAll,
+                                             int Nv, int Nr, int Nc, int P, int logP, int s0, int ns,
                                              const float* __restrict__ Hhat,
                                              const float2* __restrict__ tw,
                                              float* __restrict__ Q, int Kc) {
     extern __shared__ float2 z[];  // [npair][P]
-    const int v = blockIdx.x, rl = blockIdx.y, r = s0 + rl;
+    // blockIdx.y = chunk * ns + slice: channel chunk of Kc channels, slice of the window
+    const int v = blockIdx.x, rl = blockIdx.y % ns, chunk = blockIdx.y / ns, r = s0 + rl;
+    in += (int64_t)chunk * Kc;
+    const int Nch = min(Kc, NchAll - chunk * Kc);
     const int npair = (Nch + 1) >> 1;
     const int tid = threadIdx.x;
     const int64_t row0 = ((int64_t)v * Nr + r) * Nc;
     // load, zero-padded, into bit-reversed positions (DIT input order)
+    // channel pairs fastest: consecutive threads read consecutive channels of one detector bin
     for (int i = tid; i < npair * P; i += RT) {
-        const int pr = i / P, c = i - pr * P;
+        const int c = i / npair, pr = i - c * npair;
         float2 val = make_float2(0.f, 0.f);
         if (c < Nc) {
             const float* src = in + (row0 + c) * ld_in;
@@ -96,8 +117,8 @@ __global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64
         __syncthreads();
     }
     // store q[c], c < Nc: Q[rl][v][c][Kc]
-    float* dst = Q + (((int64_t)rl * Nv + v) * Nc) * Kc;
-    for (int i = tid; i < Nc * Kc; i += RT) {
+    float* dst = Q + ((((int64_t)chunk * ns + rl) * Nv + v) * Nc) * Kc;
+    for (int i = tid; i < Nc * Kc; i += RT) {  // channels fastest: coalesced stores
         const int c = i / Kc, ch = i - c * Kc;
         float val = 0.f;
         if (ch < Nch) {
@@ -110,22 +131,28 @@ __global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64
 
 template <int KC>
 __global__ void __launch_bounds__(TILE * TILE) k_backproject(
-    const float* __restrict__ Q, int Nch, int Nv, int Nc, int s0, const float* __restrict__ cos_t,
+    const float* __restrict__ Q, int NchAll, int Nv, int Nc, int s0, int ns, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, int mode, float* __restrict__ out, int64_t ld_out, int64_t col0,
     int64_t Nx, int vchunk) {
-    extern __shared__ __align__(16) float Qs[];  // [vchunk][WMAX][KC]
+    // [vchunk][WMAX][SP]: one detector sample's KC channels, padded so that the samples
+    // read by a quarter-warp's LDS.128 fall in distinct 16-byte bank groups
+    constexpr int SP = bp_pitch(KC);
+    extern __shared__ __align__(16) float Qs[];
     __shared__ int clo[64];
     const int tx = threadIdx.x % TILE, ty = threadIdx.x / TILE;
     const int j = blockIdx.x * TILE + tx, i = blockIdx.y * TILE + ty;
-    const int rl = blockIdx.z, r = s0 + rl;
+    // blockIdx.z = chunk * ns + slice (channel chunk of KC, slice of the window)
+    const int rl = blockIdx.z % ns, chunk = blockIdx.z / ns, r = s0 + rl;
+    const int Nch = min(KC, NchAll - chunk * KC);
+    col0 += (int64_t)chunk * KC;
     const float half = 0.5f * (float)(Nc - 1);
     const float x = (float)j - half, y = (float)i - half;
     const float xa = (float)(blockIdx.x * TILE) - half, ya = (float)(blockIdx.y * TILE) - half;
     const float xb = xa + (TILE - 1), yb = ya + (TILE - 1);
-    float acc[KC];
+    float2 acc[KC / 2];  // channel pairs; (1 - w) a + w b as two packed FMAs per pair
 #pragma unroll
-    for (int c = 0; c < KC; ++c) acc[c] = 0.f;
-    const float* Qr = Q + (int64_t)rl * Nv * Nc * KC;
+    for (int c = 0; c < KC / 2; ++c) acc[c] = make_float2(0.f, 0.f);
+    const float* Qr = Q + ((int64_t)chunk * ns + rl) * Nv * Nc * KC;
     for (int v0 = 0; v0 < Nv; v0 += vchunk) {
         const int nv = min(vchunk, Nv - v0);
         __syncthreads();
@@ -149,24 +176,22 @@ __global__ void __launch_bounds__(TILE * TILE) k_backproject(
             float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
             if (c >= 0 && c < Nc)
                 val = __ldg(reinterpret_cast<const float4*>(Qr + ((int64_t)(v0 + vv) * Nc + c) * KC) + c4);
-            reinterpret_cast<float4*>(Qs + (vv * WMAX + w) * KC)[c4] = val;
+            reinterpret_cast<float4*>(Qs + (vv * WMAX + w) * SP)[c4] = val;
         }
         __syncthreads();
         for (int vv = 0; vv < nv; ++vv) {
             const int v = v0 + vv;
             const float u = fmaf(x, cos_t[v], fmaf(y, sin_t[v], half));
             const float fl = floorf(u);
-            const float wt = u - fl;
+            const float wt = u - fl, w1 = 1.f - wt;
             const int li = (int)fl - clo[vv];
-            const float4* q0 = reinterpret_cast<const float4*>(Qs + (vv * WMAX + li) * KC);
-            const float4* q1 = q0 + KC / 4;
+            const float4* q0 = reinterpret_cast<const float4*>(Qs + (vv * WMAX + li) * SP);
+            const float4* q1 = q0 + SP / 4;
 #pragma unroll
             for (int c4 = 0; c4 < KC / 4; ++c4) {
                 const float4 a = q0[c4], b = q1[c4];
-                acc[4 * c4 + 0] += fmaf(wt, b.x - a.x, a.x);
-                acc[4 * c4 + 1] += fmaf(wt, b.y - a.y, a.y);
-                acc[4 * c4 + 2] += fmaf(wt, b.z - a.z, a.z);
-                acc[4 * c4 + 3] += fmaf(wt, b.w - a.w, a.w);
+                acc[2 * c4 + 0] = ffma2s(wt, make_float2(b.x, b.y), ffma2s(w1, make_float2(a.x, a.y), acc[2 * c4 + 0]));
+                acc[2 * c4 + 1] = ffma2s(wt, make_float2(b.z, b.w), ffma2s(w1, make_float2(a.z, a.w), acc[2 * c4 + 1]));
             }
         }
     }
@@ -177,12 +202,12 @@ __global__ void __launch_bounds__(TILE * TILE) k_backproject(
         const int64_t n = (int64_t)r * Nc * Nc + (int64_t)i * Nc + j;
 #pragma unroll
         for (int c = 0; c < KC; ++c)
-            if (c < Nch) out[(int64_t)c * Nx + n] = acc[c] * scale;
+            if (c < Nch) out[(int64_t)c * Nx + n] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
     } else {
         float* o = out + vox * ld_out + col0;
 #pragma unroll
         for (int c = 0; c < KC; ++c)
-            if (c < Nch) o[c] = acc[c] * scale;
+            if (c < Nch) o[c] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
     }
 }
 
@@ -191,15 +216,16 @@ __global__ void __launch_bounds__(TILE * TILE) k_backproject(
 cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* in, int64_t ld_in,
                         int Nch, int s0, int ns, float* Q, int Kc, cudaStream_t s) {
     if (ns <= 0) return cudaSuccess;
-    const int npair = (Nch + 1) / 2;
+    const int npair = (std::min(Nch, Kc) + 1) / 2;
     const size_t smem = (size_t)npair * g.P * sizeof(float2);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_ramp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    dim3 grid(g.Nv, ns);
-    k_ramp<<<grid, RT, smem, s>>>(in, ld_in, Nch, g.Nv, g.Nr, g.Nc, g.P, g.logP, s0, t.Hhat, t.twiddle,
+    const int nchunk = (Nch + Kc - 1) / Kc;
+    dim3 grid(g.Nv, ns * nchunk);
+    k_ramp<<<grid, RT, smem, s>>>(in, ld_in, Nch, g.Nv, g.Nr, g.Nc, g.P, g.logP, s0, ns, t.Hhat, t.twiddle,
                                   Q, Kc);
     return cudaGetLastError();
 }
@@ -207,7 +233,7 @@ cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* i
 template <int KC>
 static cudaError_t bp_k(const Geometry& g, const DeviceTables& t, const float* Q, int Nch, int s0,
                         int ns, int mode, float* out, int64_t ld_out, int64_t col0, cudaStream_t s) {
-    const int per_view = WMAX * KC * (int)sizeof(float);
+    const int per_view = WMAX * bp_pitch(KC) * (int)sizeof(float);
     int vchunk = std::min(std::min(g.Nv, 64), std::max(1, (96 * 1024) / per_view));
     const size_t smem = (size_t)vchunk * per_view;
     static bool attr = false;
@@ -215,8 +241,9 @@ static cudaError_t bp_k(const Geometry& g, const DeviceTables& t, const float* Q
         cudaFuncSetAttribute(k_backproject<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    dim3 grid((g.Nc + TILE - 1) / TILE, (g.Nc + TILE - 1) / TILE, ns);
-    k_backproject<KC><<<grid, TILE * TILE, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, t.cos_t, t.sin_t, mode,
+    const int nchunk = (Nch + KC - 1) / KC;
+    dim3 grid((g.Nc + TILE - 1) / TILE, (g.Nc + TILE - 1) / TILE, ns * nchunk);
+    k_backproject<KC><<<grid, TILE * TILE, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode,
                                                      out, ld_out, col0,
                                                      (int64_t)g.Nr * g.Nc * g.Nc, vchunk);
     return cudaGetLastError();

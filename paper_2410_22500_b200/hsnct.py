@@ -209,8 +209,8 @@ class Hsnct:
             Xh = torch.empty((n_slices * self.Nc * self.Nc, n_bins), dtype=torch.float32, device=self.device)
         ld = self._rows(Xh, "Xh", n_slices * self.Nc * self.Nc, n_bins) if Xh.numel() else max(n_bins, 1)
         if ws is None:
-            per = self.workspace_bytes(OP_DHR)
-            ws = self.workspace(OP_DHR, per * max(1, min(n_slices, 64)))
+            per = self.workspace_bytes(OP_DHR)  # one slice, all bins
+            ws = self.workspace(OP_DHR, per * max(1, min(n_slices, 8)))
         _check(lib().hsnct_dhr(self._h, _ptr(Y), ld_y, slice0, n_slices, bin0, n_bins, _ptr(Xh), ld,
                                _ptr(ws), ws.numel() * ws.element_size(), _stream(stream, self.device)))
         return Xh

@@ -268,6 +268,22 @@ def test_dhr_parity(H, cfg, window):
     assert rel(Xh, Xo) <= 1e-4, rel(Xh, Xo)
 
 
+@pytest.mark.parametrize("ws_chunk_slices", [1, 3])
+def test_dhr_small_workspace(H, ws_chunk_slices):
+    """A workspace of a few (16-bin chunk x slice) units: hsnct_dhr runs several passes."""
+    import paper_2410_22500_b200.hsnct as hm
+    cfg = sd.custom(idx=21, Nc=40, Nv=16, Nr=3, Nk=70, K=2)
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    per_chunk = cfg.Nv * cfg.Nc * 16 * 4
+    assert h.workspace_bytes(hm.OP_DHR) == per_chunk * 5  # one slice, all bins (5 chunks of 16)
+    ws = torch.empty(per_chunk * ws_chunk_slices, dtype=torch.uint8, device=DEV)
+    Xh = h.dhr(padded(pr["Y"], 72), 0, 3, 1, 67, ws=ws)
+    torch.cuda.synchronize()
+    Xo = oracle.dhr(pr["Y"].numpy(), cfg.Nv, cfg.Nr, cfg.Nc, slice0=0, n_slices=3, bin0=1, n_bins=67)
+    assert rel(Xh, Xo) <= 1e-4, rel(Xh, Xo)
+
+
 def test_linearity_identity_on_gpu(H):
     """Y = V D exactly: fbp + synthesize == dhr."""
     cfg = sd.custom(idx=21, Nc=40, Nv=30, Nr=2, Nk=23, K=3)
