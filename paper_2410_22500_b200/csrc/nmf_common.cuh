@@ -86,10 +86,10 @@ __device__ __forceinline__ void grid_sync(unsigned* count, unsigned& epoch) {
 }
 
 // s = sum over cc = q, q + NQ, ... < nC of ld(cc), in that order, with the loads issued
-// in predicated batches of 16 so that they are all in flight together.
+// in predicated batches of 24 so that they are all in flight together.
 template <class F>
 __device__ __forceinline__ double batched_sum(int q, int NQ, int nC, F&& ld) {
-    constexpr int MB = 16;
+    constexpr int MB = 24;
     double s = 0.0;
     for (int base = q; base < nC; base += NQ * MB) {
         double v[MB];

@@ -303,7 +303,7 @@ struct Pass {
                     vg = fmaf(vj, sh.Gs[j * K + k], vg);
                     if (j == k) vome = vj;
                 }
-                rfac = __fdiv_rn(vome, fmaxf(vg, 1e-30f));
+                rfac = __fdividef(vome, fmaxf(vg, 1e-30f));  // 2 ulp, no slow path (vg >= 1e-30)
             }
             // ---- phase 1: row partials of A = Y+ D^T over this thread's lambda pairs
             // p2[r][kp] = (A[r][2kp], A[r][2kp+1]) partials; per lambda one packed FFMA2
