@@ -73,6 +73,15 @@ def lib():
             L.oracle_synthesize.restype = _int
             L.oracle_synthesize.argtypes = [_f64p, _f64p, _i64, _i64, _i64, _int, _i64, _i64,
                                             _i64, _i64, _f64p, _int]
+            L.oracle_fmd_transform.restype = _int
+            L.oracle_fmd_transform.argtypes = [_f64p, _i64, _int, ctypes.POINTER(ctypes.c_int32), _int, _f64p,
+                                               _i64p]
+            L.oracle_nnls.restype = _int
+            L.oracle_nnls.argtypes = [_f64p, _int, _int, _f64p, _f64p]
+            L.oracle_fmd_materials.restype = ctypes.c_int64
+            L.oracle_fmd_materials.argtypes = [_f64p, _i64, _int, _f64p, _int, _f64p, _int]
+            L.oracle_fmd_spectra.restype = None
+            L.oracle_fmd_spectra.argtypes = [_f64p, _i64, _int, _f64p, _int, _f64p]
             L.oracle_dhr.restype = _int
             L.oracle_dhr.argtypes = [_f32p, _i64, _i64, _i64, _i64, _i64, _f64p, _i64, _i64,
                                      _i64, _i64, _f64p, _int]
@@ -235,3 +244,58 @@ def dhr(Y, Nv, Nr, Nc, angles=None, slice0=0, n_slices=None, bin0=0, n_bins=None
                         n_bins, _p64(Xh), int(nthreads)):
         raise ValueError("oracle_dhr: bad window")
     return Xh
+
+
+# ------------------------------------------------------------------ FMD (NEXT-2)
+def fmd_transform(X, labels, n_mat):
+    """Eq. 7: T [Nm, K] region means of X [K, ...] (labels < 0: no region); counts [Nm]."""
+    X = _f64(X)
+    K = X.shape[0]
+    X2 = np.ascontiguousarray(X.reshape(K, -1))
+    Nx = X2.shape[1]
+    lab = np.ascontiguousarray(np.asarray(labels).reshape(-1), dtype=np.int32)
+    assert lab.size == Nx
+    T = np.zeros((n_mat, K))
+    counts = np.zeros(n_mat, dtype=np.int64)
+    rc = lib().oracle_fmd_transform(_p64(X2), Nx, K, lab.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                    int(n_mat), _p64(T), counts.ctypes.data_as(_i64p))
+    if rc == 1:
+        raise ValueError("fmd_transform: label out of range")
+    if rc == 2:
+        raise ValueError("fmd_transform: empty region")
+    return T, counts
+
+
+def nnls(A, y):
+    """Lawson-Hanson NNLS (oracle.c: oracle_nnls): argmin_{x>=0} ||A x - y||."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    rows, m = A.shape
+    x = np.zeros(m)
+    it = lib().oracle_nnls(_p64(A), rows, m, _p64(y), _p64(x))
+    if it < 0:
+        raise ValueError("nnls failed")
+    return x
+
+
+def fmd_materials(X, T, nthreads=0):
+    """Eq. 8: Xm [Nm, ...] = per-voxel NNLS of X [K, ...] against T [Nm, K]."""
+    X = _f64(X)
+    T = _f64(T)
+    K = X.shape[0]
+    X2 = np.ascontiguousarray(X.reshape(K, -1))
+    Nm = T.shape[0]
+    Xm = np.zeros((Nm, X2.shape[1]))
+    fails = lib().oracle_fmd_materials(_p64(X2), X2.shape[1], K, _p64(T), Nm, _p64(Xm), int(nthreads))
+    if fails:
+        raise ValueError(f"fmd_materials: NNLS failed on {fails} voxels")
+    return Xm.reshape((Nm,) + X.shape[1:])
+
+
+def fmd_spectra(D, T):
+    """Eq. 9: (D^m)^T [Nm, Nk] = T [Nm, K] D [K, Nk]."""
+    D = _f64(D)
+    T = _f64(T)
+    Dm = np.zeros((T.shape[0], D.shape[1]))
+    lib().oracle_fmd_spectra(_p64(D), D.shape[1], D.shape[0], _p64(T), T.shape[0], _p64(Dm))
+    return Dm

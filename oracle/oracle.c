@@ -414,3 +414,179 @@ int oracle_dhr(const float* Y, int64_t ld_y, int64_t Nv, int64_t Nr, int64_t Nc,
         }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Fast material decomposition, semi-supervised back half (*/
+/* Section "Fast Material Decomposition", Algorithm 2), on the subspace      */
+/* reconstructions x^s (stored channel-planar X[K][Nx], reading R10).        */
+/* ------------------------------------------------------------------------ */
+
+/* Transformation matrix, Eq. 7:
+ *   T[i][j] = (1/|M_i|) sum_{n in M_i} x^s[n][j],
+ * with the regions M_i given as labels[n] = i (labels < 0: no region).
+ * counts[i] = |M_i|.  Returns 1 on a bad label, 2 if some region is empty. */
+int oracle_fmd_transform(const double* X, int64_t Nx, int K, const int32_t* labels, int Nm, double* T,
+                         int64_t* counts) {
+    for (int i = 0; i < Nm; ++i) {
+        counts[i] = 0;
+        for (int j = 0; j < K; ++j) T[i * K + j] = 0.0;
+    }
+    for (int64_t n = 0; n < Nx; ++n) {
+        const int32_t i = labels[n];
+        if (i < 0) continue;
+        if (i >= Nm) return 1;
+        counts[i] += 1;
+        for (int j = 0; j < K; ++j) T[i * K + j] += X[(int64_t)j * Nx + n];
+    }
+    for (int i = 0; i < Nm; ++i) {
+        if (counts[i] == 0) return 2;
+        for (int j = 0; j < K; ++j) T[i * K + j] /= (double)counts[i];
+    }
+    return 0;
+}
+
+/* Solve the m x m system A z = r (A row-major, copied) by Gaussian elimination with
+ * partial pivoting.  Returns 1 if singular. */
+static int solve_small(const double* A, const double* r, int m, double* z) {
+    double M[64 * 65];
+    for (int i = 0; i < m; ++i) {
+        for (int j = 0; j < m; ++j) M[i * (m + 1) + j] = A[i * m + j];
+        M[i * (m + 1) + m] = r[i];
+    }
+    for (int c = 0; c < m; ++c) {
+        int p = c;
+        for (int i = c + 1; i < m; ++i)
+            if (fabs(M[i * (m + 1) + c]) > fabs(M[p * (m + 1) + c])) p = i;
+        if (M[p * (m + 1) + c] == 0.0) return 1;
+        if (p != c)
+            for (int j = 0; j <= m; ++j) {
+                double t = M[c * (m + 1) + j];
+                M[c * (m + 1) + j] = M[p * (m + 1) + j];
+                M[p * (m + 1) + j] = t;
+            }
+        for (int i = c + 1; i < m; ++i) {
+            double f = M[i * (m + 1) + c] / M[c * (m + 1) + c];
+            for (int j = c; j <= m; ++j) M[i * (m + 1) + j] -= f * M[c * (m + 1) + j];
+        }
+    }
+    for (int i = m - 1; i >= 0; --i) {
+        double s = M[i * (m + 1) + m];
+        for (int j = i + 1; j < m; ++j) s -= M[i * (m + 1) + j] * z[j];
+        z[i] = s / M[i * (m + 1) + i];
+    }
+    return 0;
+}
+
+/* Non-negative least squares min_{x >= 0} ||A x - y||_2 for A (rows x m, row-major),
+ * following Lawson & Hanson, "Solving Least Squares Problems" (1974), Ch. 23,
+ * Algorithm NNLS (the algorithm named by Eq. 8: argmin_{x>=0}).
+ * Working on the normal equations (A^T A) x = A^T y restricted to the passive set.
+ * m <= 64.  x (m) out.  Returns the number of outer iterations, or -1 on failure. */
+int oracle_nnls(const double* A, int rows, int m, const double* y, double* x) {
+    double AtA[64 * 64], Aty[64], z[64], sub[64 * 64], rhs[64];
+    int P[64];
+    if (m < 1 || m > 64) return -1;
+    for (int i = 0; i < m; ++i) {
+        x[i] = 0.0;
+        P[i] = 0;
+        double s = 0.0;
+        for (int r = 0; r < rows; ++r) s += A[r * m + i] * y[r];
+        Aty[i] = s;
+        for (int j = 0; j < m; ++j) {
+            double t = 0.0;
+            for (int r = 0; r < rows; ++r) t += A[r * m + i] * A[r * m + j];
+            AtA[i * m + j] = t;
+        }
+    }
+    double amax = 0.0;
+    for (int i = 0; i < m; ++i) amax = fabs(Aty[i]) > amax ? fabs(Aty[i]) : amax;
+    const double tol = 1e-13 * amax + 1e-300; /* w_i > tol: a real improvement direction */
+    int outer = 0;
+    for (; outer < 3 * m + 3; ++outer) {
+        /* step 2: w = A^T (y - A x) */
+        int t = -1;
+        double wmax = 0.0;
+        for (int i = 0; i < m; ++i) {
+            double s = Aty[i];
+            for (int j = 0; j < m; ++j) s -= AtA[i * m + j] * x[j];
+            if (!P[i] && s > tol && s > wmax) {
+                wmax = s;
+                t = i;
+            }
+        }
+        if (t < 0) return outer; /* step 3: KKT satisfied */
+        P[t] = 1;                /* step 5 */
+        for (;;) {
+            /* step 6: z = LS solution on the passive set, 0 elsewhere */
+            int idx[64], np = 0;
+            for (int i = 0; i < m; ++i)
+                if (P[i]) idx[np++] = i;
+            for (int a = 0; a < np; ++a) {
+                rhs[a] = Aty[idx[a]];
+                for (int b = 0; b < np; ++b) sub[a * np + b] = AtA[idx[a] * m + idx[b]];
+            }
+            double zp[64];
+            if (solve_small(sub, rhs, np, zp)) return -1;
+            for (int i = 0; i < m; ++i) z[i] = 0.0;
+            for (int a = 0; a < np; ++a) z[idx[a]] = zp[a];
+            /* step 7: all passive z > 0 -> accept */
+            int ok = 1;
+            for (int a = 0; a < np; ++a)
+                if (z[idx[a]] <= 0.0) ok = 0;
+            if (ok) {
+                for (int i = 0; i < m; ++i) x[i] = z[i];
+                break;
+            }
+            /* steps 8-11: move towards z until a passive variable hits 0 */
+            double alpha = 1e300;
+            for (int a = 0; a < np; ++a) {
+                const int i = idx[a];
+                if (z[i] <= 0.0) {
+                    const double al = x[i] / (x[i] - z[i]);
+                    if (al < alpha) alpha = al;
+                }
+            }
+            for (int i = 0; i < m; ++i) x[i] += alpha * (z[i] - x[i]);
+            for (int a = 0; a < np; ++a) {
+                const int i = idx[a];
+                if (fabs(x[i]) <= 1e-15) {
+                    x[i] = 0.0;
+                    P[i] = 0;
+                }
+            }
+        }
+    }
+    return outer;
+}
+
+/* Material estimation, Eq. 8: for every voxel n,
+ *   x^m[n] = argmin_{x >= 0} || x^s[n] - x T ||^2,
+ * i.e. NNLS with A = T^T (K x Nm) and y = x^s[n] (K).  Xm out: [Nm][Nx] material-planar.
+ * Returns the number of voxels where NNLS failed. */
+int64_t oracle_fmd_materials(const double* X, int64_t Nx, int K, const double* T, int Nm, double* Xm,
+                             int nthreads) {
+    set_threads(nthreads);
+    double At[64 * 8];
+    for (int j = 0; j < K; ++j)
+        for (int i = 0; i < Nm; ++i) At[j * Nm + i] = T[i * K + j];
+    int64_t fails = 0;
+#pragma omp parallel for schedule(static) reduction(+ : fails)
+    for (int64_t n = 0; n < Nx; ++n) {
+        double y[64], x[8];
+        for (int j = 0; j < K; ++j) y[j] = X[(int64_t)j * Nx + n];
+        if (oracle_nnls(At, K, Nm, y, x) < 0) fails += 1;
+        for (int i = 0; i < Nm; ++i) Xm[(int64_t)i * Nx + n] = x[i];
+    }
+    return fails;
+}
+
+/* mu-spectra estimation, Eq. 9: D^m = D^s T^T.  With D stored as
+ * (D^s)^T [K][Nk], the output is (D^m)^T [Nm][Nk]:  Dm[i][l] = sum_k T[i][k] D[k][l]. */
+void oracle_fmd_spectra(const double* D, int64_t Nk, int K, const double* T, int Nm, double* Dm) {
+    for (int i = 0; i < Nm; ++i)
+        for (int64_t l = 0; l < Nk; ++l) {
+            double s = 0.0;
+            for (int k = 0; k < K; ++k) s += T[i * K + k] * D[(int64_t)k * Nk + l];
+            Dm[(int64_t)i * Nk + l] = s;
+        }
+}
