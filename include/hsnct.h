@@ -83,7 +83,8 @@ typedef enum {
     HSNCT_OP_DECOMPOSE = 0, /* hsnct_subspace_decompose                    */
     HSNCT_OP_FBP = 1,       /* hsnct_fbp                                   */
     HSNCT_OP_DHR = 2,       /* hsnct_dhr, any window (the minimum is used) */
-    HSNCT_OP_FHR_HOST = 3   /* hsnct_fhr_host                              */
+    HSNCT_OP_FHR_HOST = 3,  /* hsnct_fhr_host                              */
+    HSNCT_OP_FMD = 4        /* hsnct_fmd_transform / hsnct_fmd_materials   */
 } hsnct_op;
 
 typedef struct {
@@ -153,6 +154,31 @@ hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int 
 hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
                             const float* D0_host, int n_iter, float* Xh_host, float* V_host,
                             float* D_host, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- Fast material decomposition, semi-supervised back half (NEXT-2):
+ * Algorithm 2 after the subspace reconstruction, on X
+ * [K][N_x] (hsnct_fbp's output).  1 <= n_mat <= min(K, 8).  Workspace:
+ * hsnct_workspace_bytes(h, HSNCT_OP_FMD) (device, 256-byte aligned).
+ *
+ * Transformation matrix, Eq. 7: T[i][j] = mean of X[j][n]
+ * over the voxels n with labels[n] == i (labels: DEVICE int32 [N_x], values
+ * -1 (no region) or 0..n_mat-1, the user-provided homogeneous regions M_i).
+ * T: DEVICE fp32 [n_mat][K].  Deferred errors (hsnct_sync): a label >= n_mat or
+ * an empty region -> HSNCT_E_DATA. */
+hsnct_status hsnct_fmd_transform(hsnct_t h, const float* X, const int32_t* labels, int n_mat, float* T,
+                                 void* ws, size_t ws_bytes, void* stream);
+
+/* Material estimation, Eq. 8: for every voxel n,
+ * Xm[:, n] = argmin_{x >= 0} || X[:, n] - T^T x ||_2 (non-negative least
+ * squares, exact KKT solution).  Xm: DEVICE fp32 [n_mat][N_x] (material-planar).
+ * A singular T T^T -> HSNCT_E_NUMERIC (deferred). */
+hsnct_status hsnct_fmd_materials(hsnct_t h, const float* X, const float* T, int n_mat, float* Xm,
+                                 void* ws, size_t ws_bytes, void* stream);
+
+/* mu-spectra estimation, Eq. 9: D^m = D^s T^T, i.e. with D
+ * stored as (D^s)^T [K][N_k]:  Dm[i][l] = sum_k T[i][k] D[k][l],  Dm: DEVICE fp32
+ * [n_mat][N_k]. */
+hsnct_status hsnct_fmd_spectra(hsnct_t h, const float* D, const float* T, int n_mat, float* Dm, void* stream);
 
 /* Waits for the stream, then returns and clears the deferred status
  * (HSNCT_OK, HSNCT_E_DATA or HSNCT_E_NUMERIC), or HSNCT_E_CUDA. */

@@ -363,6 +363,7 @@ size_t hsnct_workspace_bytes(hsnct_t h, int op) {
         case HSNCT_OP_FBP: return fbp_ws(h->g);
         case HSNCT_OP_DHR: return a256(dhr_ws_per_slice(h->g));
         case HSNCT_OP_FHR_HOST: return fhr_layout(h->g, h->nmf).total;
+        case HSNCT_OP_FMD: return fmd_ws_bytes(h->g);
         default: return 0;
     }
 }
@@ -523,6 +524,72 @@ hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const 
     if (D_host)
         CK(cudaMemcpyAsync(D_host, Dd, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_host D2H D");
     return read_status(h, s);
+}
+
+static hsnct_status check_nmat(const Geometry& g, int n_mat, const char* op) {
+    if (n_mat < 1 || n_mat > std::min(g.K, 8))
+        return fail(HSNCT_E_ARG, "%s: n_mat=%d outside [1, min(K=%d, 8)]", op, n_mat, g.K);
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_fmd_transform(hsnct_t h, const float* X, const int32_t* labels, int n_mat, float* T,
+                                 void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fmd_transform: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_nmat(g, n_mat, "fmd_transform");
+    if (st) return st;
+    if (!X || !labels || !T) return fail(HSNCT_E_ARG, "fmd_transform: X, labels or T is NULL");
+    if (!aligned(X, 4) || !aligned(labels, 4) || !aligned(T, 4))
+        return fail(HSNCT_E_ARG, "fmd_transform: X, labels, T must be 4-byte aligned");
+    if ((st = check_ws(ws, ws_bytes, fmd_ws_bytes(g), "fmd_transform"))) return st;
+    const Range rT = rng(T, (size_t)n_mat * g.K * sizeof(float));
+    if (overlap(rT, rng(X, (size_t)Nx_of(g) * g.K * sizeof(float))) ||
+        overlap(rT, rng(labels, (size_t)Nx_of(g) * sizeof(int32_t))) || overlap(rT, rng(ws, ws_bytes)))
+        return fail(HSNCT_E_ARG, "fmd_transform: T must not overlap X, labels or the workspace");
+    DeviceGuard guard(h->device);
+    CK(fmd_transform(g, X, labels, n_mat, T, ws, h->t.status, (cudaStream_t)stream), "fmd_transform");
+    h->launches += 1 + (n_mat + std::max(1, std::min(8, 48 / g.K)) - 1) / std::max(1, std::min(8, 48 / g.K));
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_fmd_materials(hsnct_t h, const float* X, const float* T, int n_mat, float* Xm,
+                                 void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fmd_materials: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_nmat(g, n_mat, "fmd_materials");
+    if (st) return st;
+    if (!X || !T || !Xm) return fail(HSNCT_E_ARG, "fmd_materials: X, T or Xm is NULL");
+    if (!aligned(X, 4) || !aligned(T, 4) || !aligned(Xm, 4))
+        return fail(HSNCT_E_ARG, "fmd_materials: X, T, Xm must be 4-byte aligned");
+    if ((st = check_ws(ws, ws_bytes, fmd_ws_bytes(g), "fmd_materials"))) return st;
+    const Range rXm = rng(Xm, (size_t)n_mat * Nx_of(g) * sizeof(float));
+    if (overlap(rXm, rng(X, (size_t)Nx_of(g) * g.K * sizeof(float))) ||
+        overlap(rXm, rng(T, (size_t)n_mat * g.K * sizeof(float))) || overlap(rXm, rng(ws, ws_bytes)))
+        return fail(HSNCT_E_ARG, "fmd_materials: Xm must not overlap X, T or the workspace");
+    DeviceGuard guard(h->device);
+    CK(fmd_materials(g, X, T, n_mat, Xm, ws, h->t.status, (cudaStream_t)stream), "fmd_materials");
+    h->launches += 2;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_fmd_spectra(hsnct_t h, const float* D, const float* T, int n_mat, float* Dm, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fmd_spectra: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_nmat(g, n_mat, "fmd_spectra");
+    if (st) return st;
+    if (!D || !T || !Dm) return fail(HSNCT_E_ARG, "fmd_spectra: D, T or Dm is NULL");
+    if (!aligned(D, 4) || !aligned(T, 4) || !aligned(Dm, 4))
+        return fail(HSNCT_E_ARG, "fmd_spectra: D, T, Dm must be 4-byte aligned");
+    const Range rDm = rng(Dm, (size_t)n_mat * g.Nk * sizeof(float));
+    if (overlap(rDm, rng(D, (size_t)g.K * g.Nk * sizeof(float))) || overlap(rDm, rng(T, (size_t)n_mat * g.K * sizeof(float))))
+        return fail(HSNCT_E_ARG, "fmd_spectra: Dm must not overlap D or T");
+    DeviceGuard guard(h->device);
+    CK(fmd_spectra(g, D, T, n_mat, Dm, (cudaStream_t)stream), "fmd_spectra");
+    h->launches += 1;
+    return HSNCT_OK;
 }
 
 hsnct_status hsnct_sync(hsnct_t h, void* stream) {

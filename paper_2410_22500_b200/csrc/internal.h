@@ -125,6 +125,15 @@ cudaError_t backproject(const Geometry& g, const DeviceTables& t, const float* Q
 int ramp_launches();
 int backproject_launches();
 
+// ---------------------------------------------- FMD back half (fmd.cu, NEXT-2)
+int fmd_tblocks(const Geometry& g);
+size_t fmd_ws_bytes(const Geometry& g);
+cudaError_t fmd_transform(const Geometry& g, const float* X, const int32_t* labels, int Nm, float* T, void* ws,
+                          unsigned* status, cudaStream_t s);
+cudaError_t fmd_materials(const Geometry& g, const float* X, const float* T, int Nm, float* Xm, void* ws,
+                          unsigned* status, cudaStream_t s);
+cudaError_t fmd_spectra(const Geometry& g, const float* D, const float* T, int Nm, float* Dm, cudaStream_t s);
+
 // ------------------------------------------------------- synthesis (synth.cu)
 cudaError_t synthesize(const Geometry& g, const float* X, const float* D, int s0, int ns, int b0,
                        int nb, float* Xh, int64_t ld_xh, cudaStream_t s);

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HSNCT_LIB") or os.path.join(_HERE, "libhsnct.so")
 
 OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
-OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST = range(4)
+OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD = range(5)
 MAX_SUB = 16
 
 _lock = threading.Lock()
@@ -71,6 +71,12 @@ def lib():
             L.hsnct_status_string.restype = ctypes.c_char_p
             L.hsnct_last_error.argtypes = []
             L.hsnct_last_error.restype = ctypes.c_char_p
+            L.hsnct_fmd_transform.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
+            L.hsnct_fmd_transform.restype = i32
+            L.hsnct_fmd_materials.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
+            L.hsnct_fmd_materials.restype = i32
+            L.hsnct_fmd_spectra.argtypes = [vp, vp, vp, i32, vp, vp]
+            L.hsnct_fmd_spectra.restype = i32
             L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
             L.hsnct_debug_trace.restype = i32
             L.hsnct_abi_version.argtypes = []
@@ -233,6 +239,45 @@ class Hsnct:
                                     _ptr(Xh), _ptr(V), _ptr(D), _ptr(ws), ws.numel() * ws.element_size(),
                                     _stream(stream, self.device)))
         return Xh
+
+    # -- FMD back half (NEXT-2; Algorithm 2) ---------------------------
+    def fmd_transform(self, X, labels, n_mat, T=None, ws=None, stream=None):
+        """Eq. 7: T [n_mat, K] region means of X [K, N_r, N_c, N_c] (hsnct_fmd_transform)."""
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        if (not isinstance(labels, torch.Tensor) or labels.dtype != torch.int32 or labels.device != self.device
+                or labels.numel() != self.Nx or not labels.is_contiguous()):
+            raise HsnctError(E_ARG, f"labels must be a contiguous int32 tensor of {self.Nx} elements on {self.device}")
+        if T is None:
+            T = torch.empty((n_mat, self.K), dtype=torch.float32, device=self.device)
+        self._dev(T, "T", (n_mat, self.K))
+        ws = self.workspace(OP_FMD) if ws is None else ws
+        _check(lib().hsnct_fmd_transform(self._h, _ptr(X), _ptr(labels), int(n_mat), _ptr(T), _ptr(ws),
+                                         ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        return T
+
+    def fmd_materials(self, X, T, Xm=None, ws=None, stream=None):
+        """Eq. 8: Xm [n_mat, N_r, N_c, N_c], per-voxel NNLS (hsnct_fmd_materials)."""
+        n_mat = T.shape[0]
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        self._dev(T, "T", (n_mat, self.K))
+        if Xm is None:
+            Xm = torch.empty((n_mat, self.Nr, self.Nc, self.Nc), dtype=torch.float32, device=self.device)
+        self._dev(Xm, "Xm", (n_mat, self.Nr, self.Nc, self.Nc))
+        ws = self.workspace(OP_FMD) if ws is None else ws
+        _check(lib().hsnct_fmd_materials(self._h, _ptr(X), _ptr(T), int(n_mat), _ptr(Xm), _ptr(ws),
+                                         ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        return Xm
+
+    def fmd_spectra(self, D, T, Dm=None, stream=None):
+        """Eq. 9: (D^m)^T = T D, [n_mat, N_k] (hsnct_fmd_spectra)."""
+        n_mat = T.shape[0]
+        self._dev(D, "D", (self.K, self.Nk))
+        self._dev(T, "T", (n_mat, self.K))
+        if Dm is None:
+            Dm = torch.empty((n_mat, self.Nk), dtype=torch.float32, device=self.device)
+        self._dev(Dm, "Dm", (n_mat, self.Nk))
+        _check(lib().hsnct_fmd_spectra(self._h, _ptr(D), _ptr(T), int(n_mat), _ptr(Dm), _stream(stream, self.device)))
+        return Dm
 
     def debug_trace(self):
         """Per-iteration, per-CTA phase stamps of the last persistent decompose (ns), as a

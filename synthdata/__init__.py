@@ -318,3 +318,19 @@ def random_lowrank(Np: int, Nk: int, K: int, seed: int, device="cpu"):
     Vs = torch.rand((Np, K), generator=g, device=device, dtype=torch.float64) + 0.1
     Ds = torch.rand((K, Nk), generator=g, device=device, dtype=torch.float64) + 0.1
     return Vs, Ds
+
+
+def region_labels(pr, slices=None) -> np.ndarray:
+    """User-provided homogeneous regions for FMD's semi-supervised mode (Algorithm 2 input M,
+    PAPER.md:276-278): label m where the phantom voxel is pure material m (volume fraction 1),
+    -1 elsewhere.  int32 [Nr, Nc, Nc] (or the given slices)."""
+    cfg = pr["cfg"]
+    rs = range(cfg.Nr) if slices is None else slices
+    out = []
+    for r in rs:
+        f = rasterize(pr["shapes"], cfg, r)
+        lab = np.full((cfg.Nc, cfg.Nc), -1, np.int32)
+        for m in range(cfg.M):
+            lab[f[m] >= 1.0] = m
+        out.append(lab)
+    return np.stack(out)

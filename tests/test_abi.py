@@ -28,7 +28,8 @@ def test_header_declares_the_boundary():
     syms = declared_symbols()
     for s in ("hsnct_create", "hsnct_destroy", "hsnct_workspace_bytes", "hsnct_subspace_decompose",
               "hsnct_fbp", "hsnct_synthesize", "hsnct_dhr", "hsnct_fhr_host", "hsnct_sync",
-              "hsnct_status_string", "hsnct_last_error", "hsnct_kernel_launches", "hsnct_abi_version"):
+              "hsnct_status_string", "hsnct_last_error", "hsnct_kernel_launches", "hsnct_abi_version",
+              "hsnct_fmd_transform", "hsnct_fmd_materials", "hsnct_fmd_spectra", "hsnct_debug_trace"):
         assert s in syms
 
 
@@ -63,6 +64,9 @@ def test_null_handle_paths(L):
     assert L.hsnct_dhr(None, None, 0, 0, 0, 0, 0, None, 0, None, 0, None) == 1
     assert L.hsnct_fhr_host(None, None, 0, None, None, 0, None, None, None, None, 0, None) == 1
     assert L.hsnct_sync(None, None) == 1
+    assert L.hsnct_fmd_transform(None, None, None, 1, None, None, 0, None) == 1
+    assert L.hsnct_fmd_materials(None, None, None, 1, None, None, 0, None) == 1
+    assert L.hsnct_fmd_spectra(None, None, None, 1, None, None) == 1
     L.hsnct_destroy(None)
     del vp
 
