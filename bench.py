@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dhr", action="store_true")
+    ap.add_argument("--no-fmd", action="store_true")
     return ap.parse_args()
 
 
@@ -298,6 +299,28 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
         dhr = {"value": ns * cfg.Nc * cfg.Nc * nb / t, "unit": UNIT,
                "sample": f"{ns} slice(s) x {nb} bins, rate extrapolates linearly"}
 
+    # FMD back half (NEXT-2, outside the timed step): Eq. 7-9 on this step's X and D with the
+    # phantom's pure-material regions as the user regions
+    fmd = None
+    if not args.no_fmd and rank == 0:
+        nm = min(cfg.M, cfg.K)
+        lab = torch.as_tensor(sd.region_labels(pr), dtype=torch.int32).to(dev).contiguous()
+        T = h.fmd_transform(X, lab, nm)
+        h.fmd_materials(X, T)
+        h.fmd_spectra(D, T)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        T = h.fmd_transform(X, lab, nm)
+        Xm = h.fmd_materials(X, T)
+        Dm = h.fmd_spectra(D, T)
+        b.record(stream)
+        h.sync()
+        t = a.elapsed_time(b) * 1e-3
+        fmd = {"ms": t * 1e3, "voxels_per_s": cfg.Nx / t, "n_mat": nm,
+               "note": "transform (Eq. 7) + per-voxel NNLS (Eq. 8) + spectra (Eq. 9), not in the metric"}
+        del lab, Xm, Dm
+
     # end to end through the public API on pinned HOST buffers (hsnct_fhr_host)
     e2e = None
     if not args.no_e2e:
@@ -337,7 +360,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                            "n_iter": n_iter, "parallelism": f"replicas x{world}",
                            "l2": f"inputs larger than L2 (Y = {4 * Np * Nk / 1e6:.0f} MB > 126 MB)"},
                 "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "gpu_dhr": dhr, "clocks": clk.summary()}
+                "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

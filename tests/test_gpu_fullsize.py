@@ -85,6 +85,22 @@ def test_fullsize_sampled_parity(ci):
         h.sync()
         Xho = oracle.synthesize(X[:, r:r + 1].cpu().numpy(), D3.cpu().numpy()[:, b0:b0 + nb])
         assert rel(Xh.cpu().numpy(), Xho) <= 1e-4
+        # ---- FMD back half: T from seeded random regions (oracle on the full X), NNLS on
+        #      sampled voxels (oracle with the GPU's T), spectra
+        nm = min(cfg.M, cfg.K)
+        lab = torch.as_tensor(np.random.default_rng(ci).integers(-1, nm, cfg.Nx), dtype=torch.int32).to(DEV)
+        T = h.fmd_transform(X, lab, nm)
+        Xm = h.fmd_materials(X, T)
+        Dm = h.fmd_spectra(D3, T)
+        h.sync()
+        Xh_ = X.reshape(cfg.K, -1)
+        To, _ = oracle.fmd_transform(Xh_.cpu().numpy(), lab.cpu().numpy(), nm)
+        assert rel(T.cpu().numpy(), To) <= 1e-5
+        vox = torch.as_tensor(sample_rows(cfg.Nx, 2000, ci), device=DEV)
+        Xmo = oracle.fmd_materials(Xh_[:, vox].cpu().numpy(), T.cpu().numpy())
+        assert rel(Xm.reshape(nm, -1)[:, vox].cpu().numpy(), Xmo) <= 1e-4
+        assert rel(Dm.cpu().numpy(), oracle.fmd_spectra(D3.cpu().numpy(), T.cpu().numpy())) <= 1e-5
+        del Xh_, Xm, lab
         # ---- DHR on one slice x 8 bins
         Xd = h.dhr(Y, r, 1, 100, 8)
         h.sync()
