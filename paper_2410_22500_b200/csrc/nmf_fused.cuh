@@ -158,6 +158,7 @@ struct FusedShared {
     static constexpr int KP = (K + 3) & ~3;
     static constexpr int KK = K * K;
     uint64_t full[NGRP][NBG];
+    uint64_t part[NGRP][2];   // a group's four warp partials of a tile are in (pipelined schedule)
     unsigned rel[NGRP][NBG];
     float red[NGRP][2][GW][GK];               // per-warp row partials, by tile parity
     __align__(16) float Vn[NGRP][GW][RG][KP];  // each warp's copy of the tile's new V rows
@@ -204,6 +205,9 @@ struct Pass {
     static constexpr int DS = 2 * TG * LP;
     using Sh = FusedShared<K, NBG, NGRP>;
     static constexpr int NTH = NGRP * TG;
+    // pipelined group schedule (phase 2 of tile m - 1 overlaps the partial-sum wait of tile m)
+    // when each group has a third ring slot to prefetch into
+    static constexpr bool PIPE = NBG >= 3;
 
     const float* __restrict__ Yp;
     int64_t Np;
@@ -285,27 +289,29 @@ struct Pass {
         unsigned ph = (unsigned)((n0 / NBG) & 1);
         const int64_t rs = rstride(fwd);
         int64_t r0 = row0(g, fwd);
-        for (int64_t m = 0; m < cnt; ++m, r0 += rs) {
-            const int nv = (int)min((int64_t)RG, Np - r0);
-            mbar_wait(&sh.full[g][b], ph);
-            const float* slot = ring + (size_t)(g * NBG + b) * tf;
+        // tile of the previous iteration (PIPE: its phase 2 runs in this iteration)
+        int b_prev = 0;
+        int64_t r0_prev = 0;
+
+        // ---- phase 1 of the tile in slot `bb` (rows from r0t): V-update factor, row partials,
+        //      warp transpose-reduce, partials published in red[parity of the running count]
+        auto phase1 = [&](int bb, int64_t r0t, int nvt, int64_t ncount, float& rfac, float& vome) {
+            const float* slot = ring + (size_t)(g * NBG + bb) * tf;
             const float* yb = slot + 2 * t;
-            // ---- V-update factor V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old
-            //      V rows (lane s -> (r, k)); independent of phase 1, so its latency hides
-            float rfac = 0.f, vome = 0.f;
-            if (lane < GK) {
+            rfac = 0.f;
+            vome = 0.f;
+            if (lane < GK) {  // V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old V rows
                 const int r = lane / K, k = lane - (lane / K) * K;
                 const float* vslot = slot + (size_t)RG * Nkp;
                 float vg = 0.f;
 #pragma unroll
                 for (int j = 0; j < K; ++j) {
-                    const float vj = nv == RG ? vslot[r * K + j] : ((r < nv) ? V[(r0 + r) * K + j] : 0.f);
+                    const float vj = nvt == RG ? vslot[r * K + j] : ((r < nvt) ? V[(r0t + r) * K + j] : 0.f);
                     vg = fmaf(vj, sh.Gs[j * K + k], vg);
                     if (j == k) vome = vj;
                 }
                 rfac = __fdividef(vome, fmaxf(vg, 1e-30f));  // 2 ulp, no slow path (vg >= 1e-30)
             }
-            // ---- phase 1: row partials of A = Y+ D^T over this thread's lambda pairs
             // p2[r][kp] = (A[r][2kp], A[r][2kp+1]) partials; per lambda one packed FFMA2
             // per (r, k pair) with Y+[r][lambda] broadcast and (D[2kp][l], D[2kp+1][l])
             float2 p2[RG][KD / 2];
@@ -348,29 +354,30 @@ struct Pass {
 #pragma unroll
                 for (int k = 0; k < K; ++k) part[r * K + k] = (k & 1) ? p2[r][k >> 1].y : p2[r][k >> 1].x;
             tr_step<16, GK>(part, lane);
-            const int par = (int)(m & 1);
+            const int par = (int)(ncount & 1);
             if (((unsigned)lane & tr_bfly(GK)) == 0) {
                 const int base = tr_base<GK>(lane);
 #pragma unroll
                 for (int x = 0; x < tr_nout(GK); ++x) sh.red[g][par][wg][base + x] = part[x];
             }
-            named_bar(1 + g, TG);
-            // ---- V update, redundantly in every warp (lane s -> (r, k)): no second barrier
-            {
-                const int s = lane;
-                if (s < GK) {
-                    float a = 0.f;
+        };
+        // ---- V update of the tile (every warp redundantly, lane s -> (r, k)) once the group's
+        //      partials are in; new V rows to this warp's Vn copy, V store, <V_new, A>, H
+        auto vupdate = [&](int64_t r0t, int nvt, int64_t ncount, float rfac, float vome) {
+            const int par = (int)(ncount & 1);
+            const int s = lane;
+            if (s < GK) {
+                float a = 0.f;
 #pragma unroll
-                    for (int w = 0; w < GW; ++w) a += sh.red[g][par][w][s];
-                    float vn = a * rfac;
-                    if (s / K >= nv) vn = 0.f;
-                    sh.Vn[g][wg][s / K][s - (s / K) * K] = vn;
-                    if (wg == VWARP && s / K < nv) {
-                        if (first && !(isfinite(vome) && vome >= 0.f)) bad |= ST_INIT_BAD;
-                        if (!isfinite(vn)) bad |= ST_NUMERIC;
-                        V[r0 * K + s] = vn;
-                        vdotA += (double)vn * (double)a;
-                    }
+                for (int w = 0; w < GW; ++w) a += sh.red[g][par][w][s];
+                float vn = a * rfac;
+                if (s / K >= nvt) vn = 0.f;
+                sh.Vn[g][wg][s / K][s - (s / K) * K] = vn;
+                if (wg == VWARP && s / K < nvt) {
+                    if (first && !(isfinite(vome) && vome >= 0.f)) bad |= ST_INIT_BAD;
+                    if (!isfinite(vn)) bad |= ST_NUMERIC;
+                    V[r0t * K + s] = vn;
+                    vdotA += (double)vn * (double)a;
                 }
             }
             __syncwarp();
@@ -380,15 +387,19 @@ struct Pass {
                     const int tt = lane + 32 * x;
                     if (tt < KK) {
                         const int a = tt / K, c = tt - (tt / K) * K;
-                        double s = 0.0;
+                        double hs = 0.0;
 #pragma unroll
                         for (int r = 0; r < RG; ++r)
-                            s = fma((double)sh.Vn[g][wg][r][a], (double)sh.Vn[g][wg][r][c], s);
-                        hacc[x] += s;
+                            hs = fma((double)sh.Vn[g][wg][r][a], (double)sh.Vn[g][wg][r][c], hs);
+                        hacc[x] += hs;
                     }
                 }
             }
-            // ---- phase 2: B[k][l] += V_new[r][k] Y+[r][l]
+        };
+        // ---- phase 2 of the tile in slot `bb` with this warp's Vn copy: B[k][l] += V_new[r][k] Y+[r][l];
+        //      then the slot is released (the last warp out refills it with the tile NBG ahead)
+        auto phase2 = [&](int bb, int64_t r0t, bool refill) {
+            const float* yb = ring + (size_t)(g * NBG + bb) * tf + 2 * t;
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
                 float vr[KP];
@@ -409,24 +420,65 @@ struct Pass {
                     for (int k = 0; k < K; ++k) bacc[k][i] = ffma2(make_float2(vr[k], vr[k]), yv, bacc[k][i]);
                 }
             }
-            // ---- release the slot; the last warp out refills it with tile m + NBG
             __syncwarp();
             if (lane == 0) {
                 __threadfence_block();
                 // monotone counter: every use of a slot adds GW, so the last warp of a
                 // use sees old % GW == GW - 1 (no reset, no race with the next use)
-                if (atomicAdd(&sh.rel[g][b], 1u) % GW == GW - 1) {
-                    if (m + NBG < cnt) {
+                if (atomicAdd(&sh.rel[g][bb], 1u) % GW == GW - 1) {
+                    if (refill) {
                         fence_proxy_async();
-                        issue(g, b, r0 + NBG * rs);
+                        issue(g, bb, r0t + NBG * rs);
                     }
                 }
             }
-            if (++b == NBG) {
-                b = 0;
-                ph ^= 1u;
+        };
+
+        if constexpr (PIPE) {
+            // iteration m: phase 1 of tile m, publish its partials (split arrive), phase 2 of
+            // tile m - 1 (its V rows were updated last iteration), then wait for tile m's
+            // partials and update its V rows.  Two slots in use, NBG - 2 >= 1 prefetching.
+            for (int64_t m = 0; m <= cnt; ++m) {
+                const bool cur = m < cnt;
+                const int64_t n = n0 + m;
+                const int nv = cur ? (int)min((int64_t)RG, Np - r0) : 0;
+                float rfac = 0.f, vome = 0.f;
+                if (cur) {
+                    mbar_wait(&sh.full[g][b], ph);
+                    phase1(b, r0, nv, n, rfac, vome);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cta(&sh.part[g][n & 1]);
+                }
+                if (m > 0) phase2(b_prev, r0_prev, m - 1 + NBG < cnt);
+                if (!cur) break;
+                mbar_wait(&sh.part[g][n & 1], (unsigned)((n >> 1) & 1));
+                vupdate(r0, nv, n, rfac, vome);
+                b_prev = b;
+                r0_prev = r0;
+                r0 += rs;
+                if (++b == NBG) {
+                    b = 0;
+                    ph ^= 1u;
+                }
+            }
+        } else {
+            for (int64_t m = 0; m < cnt; ++m, r0 += rs) {
+                const int64_t n = n0 + m;
+                const int nv = (int)min((int64_t)RG, Np - r0);
+                mbar_wait(&sh.full[g][b], ph);
+                float rfac, vome;
+                phase1(b, r0, nv, n, rfac, vome);
+                named_bar(1 + g, TG);
+                vupdate(r0, nv, n, rfac, vome);
+                phase2(b, r0, m + NBG < cnt);
+                if (++b == NBG) {
+                    b = 0;
+                    ph ^= 1u;
+                }
             }
         }
+        (void)b_prev;
+        (void)r0_prev;
         // ---- per-group partials to smem
         if (wg == VWARP) {
             vdotA = warp_sum_d(vdotA);
@@ -497,6 +549,10 @@ template <int K, int NBG, int NGRP>
 __device__ __forceinline__ void fused_prologue(FusedShared<K, NBG, NGRP>& sh, float* ring, size_t ring_floats) {
     for (size_t i = threadIdx.x; i < ring_floats; i += blockDim.x) ring[i] = 0.f;
     if (threadIdx.x == 0) {
+        for (int g = 0; g < NGRP; ++g) {
+            mbar_init(&sh.part[g][0], GW);
+            mbar_init(&sh.part[g][1], GW);
+        }
         for (int g = 0; g < NGRP; ++g)
             for (int b = 0; b < NBG; ++b) {
                 mbar_init(&sh.full[g][b], 1);
