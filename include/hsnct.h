@@ -190,9 +190,9 @@ uint64_t hsnct_kernel_launches(hsnct_t h);
 
 /* Diagnostics.  When the environment variable HSNCT_TRACE=1 is set at
  * hsnct_create, the persistent decompose kernel records %globaltimer stamps (ns)
- * per iteration and CTA: [iter][cta][5] = iteration start, row pass end, first
- * grid barrier passed, D update done, iteration end (first 256 iterations of the
- * last call).  Copies min(n, available) values to the HOST buffer; *n_out
+ * per iteration and CTA: [iter][cta][8] = iteration start, row pass end, first
+ * grid barrier passed, D update done, iteration end, partials reduced, D slice
+ * updated, G reduced and D restaged (first 256 iterations of the last call).  Copies min(n, available) values to the HOST buffer; *n_out
  * receives the number available (0 when tracing is off), *n_cta the CTA count
  * (both nullable).  Synchronous. */
 hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta);

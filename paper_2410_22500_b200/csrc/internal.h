@@ -80,7 +80,8 @@ struct NmfWs {
     uint64_t* trace = nullptr;  // [trace_iters][nCTA][TRACE_SLOTS] or null
     int trace_iters = 0;
 };
-constexpr int TRACE_SLOTS = 5;   // iteration start, pass end, barrier 1, D update done, iteration end
+constexpr int TRACE_SLOTS = 8;   // iteration start, pass end, barrier 1, D update done, iteration end,
+                                 // partials reduced, D slice updated, G reduced + D restaged
 NmfPlan nmf_plan(const Geometry& g, int num_sms);
 bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p);
 size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);

@@ -719,6 +719,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
             }
             __syncthreads();
         }
+        stamp(it, 5);
         // ---- D update of the slice, <B, D_new> slice partial (fixed order)
         {
             double bd = 0.0;
@@ -757,6 +758,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
                 A.Gpart[(int64_t)c * KK + o] = s;
             }
         }
+        stamp(it, 6);
         stamp(it, 3);
         grid_sync(A.bar, epoch);
         // ---- G_new from the slice partials (every CTA, same fixed order; its loads are
@@ -797,6 +799,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
             }
             __syncthreads();
         }
+        stamp(it, 7);
         if (c == nC - 1 && (A.obj || it == 0)) {  // the objective trace (and the Y+ = 0 check)
             double v0 = 0.0, v1 = 0.0, v2 = 0.0;
             for (int i = tid; i < nC; i += NTH) {

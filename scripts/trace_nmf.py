@@ -43,10 +43,12 @@ def main():
     us = 1e-3
     rows = []
     for it in range(2, n):
-        s0, pe, b1, du, ie = (t[it, :, j] for j in range(5))
+        s0, pe, b1, du, ie, pr, ds, gr = (t[it, :, j] for j in range(8))
         rows.append(dict(
             pass_min=(pe - s0).min() * us, pass_mean=(pe - s0).mean() * us, pass_max=(pe - s0).max() * us,
             bar1=(b1.max() - pe.max()) * us, dupd=(du - b1).mean() * us, dupd_max=(du - b1).max() * us,
+            d_reduce=(pr - b1).mean() * us, d_update=(ds - pr).mean() * us, bar2=(gr.min() - du.max()) * us,
+            g_restage=(gr - du).mean() * us, objective_tail=(ie - gr).mean() * us,
             bar2_restage=(ie - du).mean() * us, iter_wall=(ie.max() - s0.min()) * us,
             start_skew=(s0.max() - s0.min()) * us))
     keys = rows[0].keys()
