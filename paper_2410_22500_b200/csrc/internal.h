@@ -48,6 +48,8 @@ struct NmfPlan {
     int LP;          // lambda pairs per thread
     int nbuf;        // ring slots per compute group
     int ngrp;        // compute groups of 4 warps (3 or 4)
+    bool rotate;     // rotate the lambda slots per group over the SM sub-partitions
+    bool l2pf;       // L2 prefetch one tile beyond the ring (per group)
     int PB;          // B partials of the fused kernel (2 per CTA)
     int nby;         // blocks of the Y+ preparation kernel
     int fthreads;    // threads per CTA

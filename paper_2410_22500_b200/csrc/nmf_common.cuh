@@ -36,6 +36,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+// Warm L2 with `bytes` (multiple of 16) at global address src, no shared-memory destination.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // Orders this thread's (and, after a barrier, the CTA's) generic-proxy shared-memory
 // accesses before its subsequent bulk copies into the same buffers.
 __device__ __forceinline__ void fence_proxy_async() {

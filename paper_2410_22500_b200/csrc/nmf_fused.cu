@@ -27,6 +27,12 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     p->LP = LP;
     p->nbuf = nbuf;
     p->ngrp = ngrp;
+    // rotating the ragged lambda slots over the SM sub-partitions measured +1% with four
+    // groups (C2) and -1% with three (C4); on by default for four groups only
+    const char* rt = getenv("HSNCT_ROTATE");
+    p->rotate = rt ? rt[0] == '1' : ngrp == 4;
+    const char* pf = getenv("HSNCT_L2PF");
+    p->l2pf = pf ? pf[0] == '1' : false;  // measured -1.6% at C4: the pass is issue-bound
     p->fthreads = ngrp * TG;
     p->smem_f = fused_smem_bytes(Nkp, g.K, LP, nbuf, ngrp);
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;

@@ -40,8 +40,8 @@ constexpr int RG = 4;              // rows per tile
 constexpr int GW = 4;              // warps per group
 constexpr int TG = GW * 32;        // threads per group
 constexpr int NTHREADS = 3 * TG;   // default CTA size (3 groups); 4 groups when registers allow
-constexpr int VWARP = GW - 1;      // warp of a group that stores V (fewest lambda pairs)
-constexpr int HWARP = GW - 2;      // warp of a group that accumulates H
+// Warp of group g that stores V / accumulates H: (g + 3) % 4 and (g + 2) % 4, never the warp
+// g % 4 that carries the ragged last lambda pairs (see the slot rotation in Pass::run).
 
 // d = a * b + c on both halves (one packed FFMA2 on sm_100a), each half rounded
 // exactly like fmaf.
@@ -218,6 +218,8 @@ struct Pass {
     Sh& sh;
     int64_t nmine;   // tiles of this CTA
     size_t tf;       // floats per tile
+    bool rotate;     // rotate the lambda slots per group (see run)
+    bool l2pf;       // L2 prefetch of the tile after the one being refilled
 
     __device__ __forceinline__ int64_t count_g(int g) const {
         return nmine > g ? (nmine - 1 - g) / NGRP + 1 : 0;
@@ -262,6 +264,12 @@ struct Pass {
                         float* __restrict__ Bout, double* __restrict__ Hout, double* __restrict__ vout) const {
         const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
         const int g = warp / GW, wg = warp - g * GW, t = tid - g * TG;
+        // lambda-slot index of this thread: the warps of group g take the slots rotated by g,
+        // so the warp that carries the ragged last lambda pairs (slots < 32) is warp g % GW --
+        // a different SM sub-partition for every group (warp w runs on sub-partition w % 4)
+        const int rot = rotate ? g % GW : 0;
+        const int tl = ((wg - rot + GW) % GW) * 32 + lane;
+        const int VWARP = (rot + GW - 1) % GW, HWARP = (rot + GW - 2) % GW;
         const int64_t cnt = count_g(g);
         if (!prefetched) {
             if (t == 0) {
@@ -270,7 +278,7 @@ struct Pass {
                 issue_head(g, n0, fwd);
             }
         }
-        const bool lastok = 2 * (t + TG * (LP - 1)) < Nkp;  // last lambda pair inside the row
+        const bool lastok = 2 * (tl + TG * (LP - 1)) < Nkp;  // last lambda pair inside the row
         float2 bacc[K][LP];
 #pragma unroll
         for (int k = 0; k < K; ++k)
@@ -297,7 +305,7 @@ struct Pass {
         //      warp transpose-reduce, partials published in red[parity of the running count]
         auto phase1 = [&](int bb, int64_t r0t, int nvt, int64_t ncount, float& rfac, float& vome) {
             const float* slot = ring + (size_t)(g * NBG + bb) * tf;
-            const float* yb = slot + 2 * t;
+            const float* yb = slot + 2 * tl;
             rfac = 0.f;
             vome = 0.f;
             if (lane < GK) {  // V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old V rows
@@ -322,7 +330,7 @@ struct Pass {
 #pragma unroll
             for (int i = 0; i < LP; ++i) {
                 const bool ok = (i < LP - 1) || lastok;
-                const int pp = t + TG * i;  // lambda pair
+                const int pp = tl + TG * i;  // lambda pair
                 float2 yy[RG];
 #pragma unroll
                 for (int r = 0; r < RG; ++r)
@@ -399,7 +407,7 @@ struct Pass {
         // ---- phase 2 of the tile in slot `bb` with this warp's Vn copy: B[k][l] += V_new[r][k] Y+[r][l];
         //      then the slot is released (the last warp out refills it with the tile NBG ahead)
         auto phase2 = [&](int bb, int64_t r0t, bool refill) {
-            const float* yb = ring + (size_t)(g * NBG + bb) * tf + 2 * t;
+            const float* yb = ring + (size_t)(g * NBG + bb) * tf + 2 * tl;
 #pragma unroll
             for (int r = 0; r < RG; ++r) {
                 float vr[KP];
@@ -429,6 +437,10 @@ struct Pass {
                     if (refill) {
                         fence_proxy_async();
                         issue(g, bb, r0t + NBG * rs);
+                        // and warm L2 with the tile after it (a third tile in flight per group
+                        // without a third shared-memory slot)
+                        const int64_t rp = r0t + (NBG + 1) * rs;
+                        if (l2pf && rp >= 0 && rp + RG <= Np) bulk_prefetch_l2(Yp + rp * Nkp, (unsigned)(RG * Nkp * sizeof(float)));
                     }
                 }
             }
@@ -503,13 +515,13 @@ struct Pass {
             if (g > 0) {
 #pragma unroll
                 for (int i = 0; i < LP; ++i)
-                    *reinterpret_cast<float2*>(comb + (g - 1) * DS + 2 * (t + TG * i)) = bacc[k][i];
+                    *reinterpret_cast<float2*>(comb + (g - 1) * DS + 2 * (tl + TG * i)) = bacc[k][i];
             }
             __syncthreads();
             if (g == 0) {
 #pragma unroll
                 for (int i = 0; i < LP; ++i) {
-                    const int l0 = 2 * (t + TG * i);
+                    const int l0 = 2 * (tl + TG * i);
                     if (l0 < Nkp) {
                         float2 o = bacc[k][i];
 #pragma unroll
@@ -587,7 +599,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_fused(const float* __restr
                                                            const double* __restrict__ Gd,
                                                            float* __restrict__ Bpart,
                                                            double* __restrict__ Hpart,
-                                                           double* __restrict__ vpart, int it,
+                                                           double* __restrict__ vpart, int it, int rotate,
                                                            unsigned* __restrict__ status) {
     using P = Pass<K, LP, NBG, NGRP>;
     constexpr int DS = P::DS;
@@ -602,7 +614,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_fused(const float* __restr
     __syncthreads();
     const int64_t ntiles = (Np + RG - 1) / RG;
     const int64_t nmine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    P pass{Yp, Np, Nkp, V, ring, Ds, sh, nmine, tf};
+    P pass{Yp, Np, Nkp, V, ring, Ds, sh, nmine, tf, (rotate & 1) != 0, (rotate & 2) != 0};
     pass.run(0, it == 0, (it & 1) == 0, false, false, false, Bpart + (int64_t)blockIdx.x * K * Nkp,
              Hpart + (int64_t)blockIdx.x * K * K, vpart + 2 * (int64_t)blockIdx.x);
     if (threadIdx.x == 0) {
@@ -631,6 +643,7 @@ struct PersistArgs {
     int trace_iters;
     unsigned* bar;   // arrival counter, zero at launch
     unsigned* status;
+    int rotate;      // bit 0: rotate the lambda slots per group; bit 1: L2 prefetch
 };
 
 // All n_iter Lee-Seung iterations in one cooperative launch.  Per iteration:
@@ -665,7 +678,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
     __syncthreads();
     const int64_t ntiles = (A.Np + RG - 1) / RG;
     const int64_t nmine = ntiles > c ? (ntiles - 1 - c) / nC + 1 : 0;
-    P pass{A.Yp, A.Np, A.Nkp, A.V, ring, Ds, sh, nmine, tf};
+    P pass{A.Yp, A.Np, A.Nkp, A.V, ring, Ds, sh, nmine, tf, (A.rotate & 1) != 0, (A.rotate & 2) != 0};
     const int g = tid / TG;
     const int64_t cnt = pass.count_g(g);
     // lambda slice of this CTA for the D update
@@ -868,7 +881,7 @@ inline cudaError_t fused_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w
     }
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     k_nmf_fused<K, LP, NB, NG><<<p.nblk_f, NG * TG, p.smem_f, s>>>(w.Yp, Np, g.Nk, p.Nkp, V, D, w.Gd, w.Bpart,
-                                                                  w.Hpart, w.vpart, it, status);
+                                                                  w.Hpart, w.vpart, it, (p.rotate ? 1 : 0) | (p.l2pf ? 2 : 0), status);
     return cudaGetLastError();
 }
 
@@ -904,6 +917,7 @@ inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs&
     A.trace_iters = w.trace_iters;
     A.bar = bar;
     A.status = status;
+    A.rotate = (p.rotate ? 1 : 0) | (p.l2pf ? 2 : 0);
     void* args[] = {&A};
     cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);  // grid-barrier arrival counter
     if (e != cudaSuccess) return e;
