@@ -345,7 +345,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                    "d2h_bytes_per_step": 4 * Nx * Nk, "ms_per_step": t_e2e * 1e3}
 
     cpu = None
-    if not args.no_cpu and rank == 0:
+    if not args.no_cpu and rank == 0 and world == 1:  # the CPU baseline: rank 0 at N = 1 only
         T, desc, cores = oracle_sample(pr, n_iter)
         cpu = {"value": cfg.Nx * cfg.Nk / T, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": desc}
