@@ -43,7 +43,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, var
           defines=()) -> str:
     """Compile and link libhsnct.so.  A non-empty variant (with extra -D defines) builds an
     experimental libhsnct_<variant>.so from separate objects (select it with HSNCT_LIB)."""
-    BUILD = os.path.join(HERE, "build" + (f"_{variant}" if variant else ""))
+    # variant objects live outside the tree (only the in-tree .so travels to the GPU box)
+    BUILD = os.path.join("/tmp", f"hsnct_build_{variant}") if variant else os.path.join(HERE, "build")
     LIB = os.path.join(HERE, f"libhsnct_{variant}.so" if variant else "libhsnct.so")
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]

@@ -27,10 +27,11 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     p->LP = LP;
     p->nbuf = nbuf;
     p->ngrp = ngrp;
-    // rotating the ragged lambda slots over the SM sub-partitions measured +1% with four
-    // groups (C2) and -1% with three (C4); on by default for four groups only
+    // rotating the ragged lambda slots over the SM sub-partitions: +1% with four groups (C2);
+    // with three groups it pays once the warps without a last lambda pair skip that slot
+    // (Pass::SKIP): C4 6.61 -> 6.24 ms per iteration (rotation alone: -1%)
     const char* rt = getenv("HSNCT_ROTATE");
-    p->rotate = rt ? rt[0] == '1' : ngrp == 4;
+    p->rotate = rt ? rt[0] == '1' : true;
     const char* pf = getenv("HSNCT_L2PF");
     p->l2pf = pf ? pf[0] == '1' : false;  // measured -1.6% at C4: the pass is issue-bound
     p->fthreads = ngrp * TG;

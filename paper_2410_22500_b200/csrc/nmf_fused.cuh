@@ -208,6 +208,10 @@ struct Pass {
     // pipelined group schedule (phase 2 of tile m - 1 overlaps the partial-sum wait of tile m)
     // when each group has a third ring slot to prefetch into
     static constexpr bool PIPE = NBG >= 3;
+    // warps none of whose lanes has a last lambda pair skip that slot (a warp-uniform branch).
+    // Three groups only: at four (128 registers) the branch measured slower than multiplying
+    // zeros (C2 49.1 -> 50.0 us per iteration), at three it pays with the slot rotation.
+    static constexpr bool SKIP = NGRP == 3;
 
     const float* __restrict__ Yp;
     int64_t Np;
@@ -279,6 +283,9 @@ struct Pass {
             }
         }
         const bool lastok = 2 * (tl + TG * (LP - 1)) < Nkp;  // last lambda pair inside the row
+        // warp-uniform: some lane of this warp has its last lambda pair inside the row (the
+        // other warps skip the last slot instead of multiplying zeros)
+        const bool wlast = 2 * (tl - lane + TG * (LP - 1)) < Nkp;
         float2 bacc[K][LP];
 #pragma unroll
         for (int k = 0; k < K; ++k)
@@ -291,6 +298,7 @@ struct Pass {
 #pragma unroll
         for (int x = 0; x < (KK + 31) / 32; ++x) hacc[x] = 0.0;
         unsigned bad = 0;
+        const unsigned fullb = smem_u32(&sh.full[g][0]), partb = smem_u32(&sh.part[g][0]);
         // running slot / mbarrier phase / first row of the group's current tile (no 64-bit
         // division or multiply per tile)
         int b = (int)(n0 % NBG);
@@ -310,13 +318,17 @@ struct Pass {
             vome = 0.f;
             if (lane < GK) {  // V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old V rows
                 const int r = lane / K, k = lane - (lane / K) * K;
-                const float* vslot = slot + (size_t)RG * Nkp;
                 float vg = 0.f;
+                if (nvt == RG) {  // warp-uniform: every tile but the ragged last one
+                    const float* vrow = slot + (size_t)RG * Nkp + r * K;
 #pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const float vj = nvt == RG ? vslot[r * K + j] : ((r < nvt) ? V[(r0t + r) * K + j] : 0.f);
-                    vg = fmaf(vj, sh.Gs[j * K + k], vg);
-                    if (j == k) vome = vj;
+                    for (int j = 0; j < K; ++j) vg = fmaf(vrow[j], sh.Gs[j * K + k], vg);
+                    vome = vrow[k];
+                } else {
+                    const bool in = r < nvt;
+#pragma unroll
+                    for (int j = 0; j < K; ++j) vg = fmaf(in ? V[(r0t + r) * K + j] : 0.f, sh.Gs[j * K + k], vg);
+                    vome = in ? V[(r0t + r) * K + k] : 0.f;
                 }
                 rfac = __fdividef(vome, fmaxf(vg, 1e-30f));  // 2 ulp, no slow path (vg >= 1e-30)
             }
@@ -329,6 +341,7 @@ struct Pass {
                 for (int kp = 0; kp < KD / 2; ++kp) p2[r][kp] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int i = 0; i < LP; ++i) {
+                if (SKIP && i == LP - 1 && !wlast) break;
                 const bool ok = (i < LP - 1) || lastok;
                 const int pp = tl + TG * i;  // lambda pair
                 float2 yy[RG];
@@ -421,6 +434,7 @@ struct Pass {
                 }
 #pragma unroll
                 for (int i = 0; i < LP; ++i) {
+                    if (SKIP && i == LP - 1 && !wlast) break;
                     const bool ok = (i < LP - 1) || lastok;
                     const float2 yv = ok ? *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i)
                                          : make_float2(0.f, 0.f);
@@ -456,14 +470,14 @@ struct Pass {
                 const int nv = cur ? (int)min((int64_t)RG, Np - r0) : 0;
                 float rfac = 0.f, vome = 0.f;
                 if (cur) {
-                    mbar_wait(&sh.full[g][b], ph);
+                    mbar_wait_s(fullb + 8u * (unsigned)b, ph);
                     phase1(b, r0, nv, n, rfac, vome);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cta(&sh.part[g][n & 1]);
                 }
                 if (m > 0) phase2(b_prev, r0_prev, m - 1 + NBG < cnt);
                 if (!cur) break;
-                mbar_wait(&sh.part[g][n & 1], (unsigned)((n >> 1) & 1));
+                mbar_wait_s(partb + 8u * (unsigned)(n & 1), (unsigned)((n >> 1) & 1));
                 vupdate(r0, nv, n, rfac, vome);
                 b_prev = b;
                 r0_prev = r0;
@@ -477,7 +491,7 @@ struct Pass {
             for (int64_t m = 0; m < cnt; ++m, r0 += rs) {
                 const int64_t n = n0 + m;
                 const int nv = (int)min((int64_t)RG, Np - r0);
-                mbar_wait(&sh.full[g][b], ph);
+                mbar_wait_s(fullb + 8u * (unsigned)b, ph);
                 float rfac, vome;
                 phase1(b, r0, nv, n, rfac, vome);
                 named_bar(1 + g, TG);
