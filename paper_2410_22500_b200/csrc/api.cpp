@@ -82,7 +82,8 @@ bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi && a.hi > a.l
 
 int64_t Np_of(const Geometry& g) { return (int64_t)g.Nv * g.Nr * g.Nc; }
 int64_t Nx_of(const Geometry& g) { return (int64_t)g.Nr * g.Nc * g.Nc; }
-int kc_of(int K) { return (K + 3) & ~3; }
+// FHR channels per filtered-sinogram sample: K exactly up to 8 (no padding in Q), else 16
+int kc_of(int K) { return K <= 8 ? K : 16; }
 int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
 
 size_t fbp_ws(const Geometry& g) { return a256((size_t)Np_of(g) * kc_of(g.K) * sizeof(float)); }

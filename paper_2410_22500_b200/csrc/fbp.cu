@@ -22,11 +22,15 @@ namespace hsnct {
 namespace {
 
 constexpr int RT = 256;      // ramp-filter threads
-constexpr int TILE = 16;     // backprojection voxel tile edge
-constexpr int WMAX = 28;     // detector window per view per tile (>= 16*sqrt(2) + 4)
-// floats per staged detector sample: KC, plus 4 when KC/4 is even (an odd number of
-// 16-byte chunks per sample spreads consecutive samples over all bank groups)
-__host__ __device__ constexpr int bp_pitch(int KC) { return KC + (((KC / 4) % 2 == 0) ? 4 : 0); }
+constexpr int BTX = 16, BTY = 32;  // backprojection voxel tile (columns x rows)
+// detector window per view per tile: the tile's voxels span <= 15|cos| + 31|sin| <= 34.4 bins,
+// plus the interpolation neighbour and a one-bin margin on each side of floor()
+constexpr int BWMAX = 40;
+constexpr int BVMAX = 64;          // views per staged chunk (upper bound)
+// floats per staged detector sample: KC, plus 4 when KC is a multiple of 8 (an odd number
+// of 16-byte chunks per sample spreads a quarter-warp's LDS.128 over all bank groups; the
+// other widths are conflict-free as they are for neighbouring samples)
+__host__ __device__ constexpr int bp_pitch(int KC) { return KC % 8 == 0 ? KC + 4 : KC; }
 
 __device__ __forceinline__ unsigned bitrev(unsigned x, int logP) { return __brev(x) >> (32 - logP); }
 
@@ -129,85 +133,159 @@ __global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64
     }
 }
 
+// cp.async of VEC floats with zero fill (src_bytes = 0 -> zeros); 4/8/16-byte forms
+template <int VEC>
+__device__ __forceinline__ void cp_async_zfill(float* dst, const float* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int n = ok ? 4 * VEC : 0;
+    if constexpr (VEC == 4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+    else if constexpr (VEC == 2)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Voxel-driven backprojection.  Block = a BTX x BTY voxel tile of one slice (and one channel
+// chunk), 256 threads, two voxels per thread (rows ty and ty + 16).  Views are processed in
+// chunks of vch: per view the tile's detector window (BWMAX samples from clo, KC channels
+// each, stored exactly as in Q so a window is one contiguous run of floats) is staged by
+// cp.async into one of two buffers while the other chunk is being used.  Per voxel and view:
+// u = x cos + y sin + (N_c - 1)/2, l = floor(u), w = u - l, acc += (1 - w) q[l] + w q[l + 1].
 template <int KC>
-__global__ void __launch_bounds__(TILE * TILE) k_backproject(
+__global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
     const float* __restrict__ Q, int NchAll, int Nv, int Nc, int s0, int ns, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, int mode, float* __restrict__ out, int64_t ld_out, int64_t col0,
-    int64_t Nx, int vchunk) {
-    // [vchunk][WMAX][SP]: one detector sample's KC channels, padded so that the samples
-    // read by a quarter-warp's LDS.128 fall in distinct 16-byte bank groups
-    constexpr int SP = bp_pitch(KC);
-    extern __shared__ __align__(16) float Qs[];
-    __shared__ int clo[64];
-    const int tx = threadIdx.x % TILE, ty = threadIdx.x / TILE;
-    const int j = blockIdx.x * TILE + tx, i = blockIdx.y * TILE + ty;
+    int64_t Nx, int vch) {
+    constexpr int NT = BTX * BTY / 2;
+    constexpr int VEC = KC % 4 == 0 ? 4 : (KC % 2 == 0 ? 2 : 1);  // floats per copy / per LDS
+    constexpr int SP = bp_pitch(KC);                               // floats per staged sample
+    constexpr int WQ = BWMAX * KC;                                 // floats per view window in Q
+    constexpr int WIN = BWMAX * SP;                                // ... and in shared memory
+    extern __shared__ __align__(16) float Ws[];                    // [2][vch][WIN]
+    __shared__ float2 csn[2][BVMAX];
+    __shared__ int clo[2][BVMAX];
+    const int tid = threadIdx.x;
+    const int tx = tid % BTX, ty = tid / BTX;
+    const int j = blockIdx.x * BTX + tx, i0 = blockIdx.y * BTY + ty;
     // blockIdx.z = chunk * ns + slice (channel chunk of KC, slice of the window)
     const int rl = blockIdx.z % ns, chunk = blockIdx.z / ns, r = s0 + rl;
     const int Nch = min(KC, NchAll - chunk * KC);
     col0 += (int64_t)chunk * KC;
     const float half = 0.5f * (float)(Nc - 1);
-    const float x = (float)j - half, y = (float)i - half;
-    const float xa = (float)(blockIdx.x * TILE) - half, ya = (float)(blockIdx.y * TILE) - half;
-    const float xb = xa + (TILE - 1), yb = ya + (TILE - 1);
-    float2 acc[KC / 2];  // channel pairs; (1 - w) a + w b as two packed FMAs per pair
-#pragma unroll
-    for (int c = 0; c < KC / 2; ++c) acc[c] = make_float2(0.f, 0.f);
+    const float x = (float)j - half, y0 = (float)i0 - half, y1 = y0 + (float)(BTY / 2);
+    const float xa = (float)(blockIdx.x * BTX) - half, ya = (float)(blockIdx.y * BTY) - half;
+    const float xb = xa + (BTX - 1), yb = ya + (BTY - 1);
     const float* Qr = Q + ((int64_t)chunk * ns + rl) * Nv * Nc * KC;
-    for (int v0 = 0; v0 < Nv; v0 += vchunk) {
-        const int nv = min(vchunk, Nv - v0);
-        __syncthreads();
-        if ((int)threadIdx.x < nv) {
-            const int v = v0 + threadIdx.x;
+    const int nchk = (Nv + vch - 1) / vch;
+
+    // view metadata of chunk ck into buffer b: (cos, sin) and the window start
+    auto meta = [&](int ck, int b) {
+        const int v = ck * vch + tid;
+        if (tid < vch && v < Nv) {
             const float cs = cos_t[v], sn = sin_t[v];
             const float u1 = fmaf(xa, cs, fmaf(ya, sn, half));
             const float u2 = fmaf(xb, cs, fmaf(ya, sn, half));
             const float u3 = fmaf(xa, cs, fmaf(yb, sn, half));
             const float u4 = fmaf(xb, cs, fmaf(yb, sn, half));
-            const float umin = fminf(fminf(u1, u2), fminf(u3, u4));
-            clo[threadIdx.x] = (int)floorf(umin) - 1;
+            clo[b][tid] = (int)floorf(fminf(fminf(u1, u2), fminf(u3, u4))) - 1;
+            csn[b][tid] = make_float2(cs, sn);
         }
-        __syncthreads();
-        // cooperative load of the per-view windows (zero outside the detector)
-        for (int t = threadIdx.x; t < nv * WMAX * (KC / 4); t += TILE * TILE) {
-            const int vv = t / (WMAX * (KC / 4));
-            const int rem = t - vv * (WMAX * (KC / 4));
-            const int w = rem / (KC / 4), c4 = rem - w * (KC / 4);
-            const int c = clo[vv] + w;
-            float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c >= 0 && c < Nc)
-                val = __ldg(reinterpret_cast<const float4*>(Qr + ((int64_t)(v0 + vv) * Nc + c) * KC) + c4);
-            reinterpret_cast<float4*>(Qs + (vv * WMAX + w) * SP)[c4] = val;
+    };
+    // windows of chunk ck into buffer b (zero outside the detector), one cp.async group
+    auto stage = [&](int ck, int b) {
+        const int v0 = ck * vch, nv = min(vch, Nv - v0);
+        float* dst = Ws + (size_t)b * vch * WIN;
+        for (int t = tid; t < nv * (WQ / VEC); t += NT) {
+            const int vv = t / (WQ / VEC), e = (t - vv * (WQ / VEC)) * VEC;
+            const int w = e / KC, c = clo[b][vv] + w;
+            const bool ok = c >= 0 && c < Nc;
+            const float* src = ok ? Qr + ((int64_t)(v0 + vv) * Nc + clo[b][vv]) * KC + e : Qr;
+            cp_async_zfill<VEC>(dst + vv * WIN + w * SP + (e - w * KC), src, ok);
         }
-        __syncthreads();
-        for (int vv = 0; vv < nv; ++vv) {
-            const int v = v0 + vv;
-            const float u = fmaf(x, cos_t[v], fmaf(y, sin_t[v], half));
-            const float fl = floorf(u);
-            const float wt = u - fl, w1 = 1.f - wt;
-            const int li = (int)fl - clo[vv];
-            const float4* q0 = reinterpret_cast<const float4*>(Qs + (vv * WMAX + li) * SP);
-            const float4* q1 = q0 + SP / 4;
+        cp_async_commit();
+    };
+
+    float2 acc0[(KC + 1) / 2], acc1[(KC + 1) / 2];
 #pragma unroll
-            for (int c4 = 0; c4 < KC / 4; ++c4) {
-                const float4 a = q0[c4], b = q1[c4];
-                acc[2 * c4 + 0] = ffma2s(wt, make_float2(b.x, b.y), ffma2s(w1, make_float2(a.x, a.y), acc[2 * c4 + 0]));
-                acc[2 * c4 + 1] = ffma2s(wt, make_float2(b.z, b.w), ffma2s(w1, make_float2(a.z, a.w), acc[2 * c4 + 1]));
+    for (int c = 0; c < (KC + 1) / 2; ++c) acc0[c] = acc1[c] = make_float2(0.f, 0.f);
+    // (1 - w) q[l] + w q[l + 1] into acc, KC channels from the window at p
+    auto interp = [&](float2* acc, const float* p, float wt) {
+        const float w1 = 1.f - wt;
+        float a[KC + 1], bq[KC + 1];
+#pragma unroll
+        for (int c = 0; c < KC; c += VEC) {
+            if constexpr (VEC == 4) {
+                const float4 qa = *reinterpret_cast<const float4*>(p + c);
+                const float4 qb = *reinterpret_cast<const float4*>(p + SP + c);
+                a[c] = qa.x; a[c + 1] = qa.y; a[c + 2] = qa.z; a[c + 3] = qa.w;
+                bq[c] = qb.x; bq[c + 1] = qb.y; bq[c + 2] = qb.z; bq[c + 3] = qb.w;
+            } else if constexpr (VEC == 2) {
+                const float2 qa = *reinterpret_cast<const float2*>(p + c);
+                const float2 qb = *reinterpret_cast<const float2*>(p + SP + c);
+                a[c] = qa.x; a[c + 1] = qa.y;
+                bq[c] = qb.x; bq[c + 1] = qb.y;
+            } else {
+                a[c] = p[c];
+                bq[c] = p[SP + c];
             }
         }
+        a[KC] = bq[KC] = 0.f;
+#pragma unroll
+        for (int c = 0; c < (KC + 1) / 2; ++c)
+            acc[c] = ffma2s(wt, make_float2(bq[2 * c], bq[2 * c + 1]),
+                            ffma2s(w1, make_float2(a[2 * c], a[2 * c + 1]), acc[c]));
+    };
+
+    meta(0, 0);
+    __syncthreads();
+    stage(0, 0);
+    for (int ck = 0; ck < nchk; ++ck) {
+        const int b = ck & 1;
+        if (ck + 1 < nchk) {  // prefetch the next chunk into the other buffer
+            meta(ck + 1, b ^ 1);
+            __syncthreads();
+            stage(ck + 1, b ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int nv = min(vch, Nv - ck * vch);
+        const float* win = Ws + (size_t)b * vch * WIN;
+        for (int vv = 0; vv < nv; ++vv) {
+            const float2 t = csn[b][vv];
+            const int cl = clo[b][vv];
+            const float u0 = fmaf(x, t.x, fmaf(y0, t.y, half));
+            const float u1 = fmaf(x, t.x, fmaf(y1, t.y, half));
+            const float f0 = floorf(u0), f1 = floorf(u1);
+            interp(acc0, win + vv * WIN + ((int)f0 - cl) * SP, u0 - f0);
+            interp(acc1, win + vv * WIN + ((int)f1 - cl) * SP, u1 - f1);
+        }
+        __syncthreads();  // buffer b is refilled by the next iteration's prefetch
     }
-    if (i >= Nc || j >= Nc) return;
+    if (j >= Nc) return;
     const float scale = 3.14159265358979323846f / (float)Nv;
-    const int64_t vox = ((int64_t)rl * Nc + i) * Nc + j;
-    if (mode == 0) {
-        const int64_t n = (int64_t)r * Nc * Nc + (int64_t)i * Nc + j;
 #pragma unroll
-        for (int c = 0; c < KC; ++c)
-            if (c < Nch) out[(int64_t)c * Nx + n] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
-    } else {
-        float* o = out + vox * ld_out + col0;
+    for (int q = 0; q < 2; ++q) {
+        const int i = i0 + q * (BTY / 2);
+        if (i >= Nc) break;
+        const float2* acc = q ? acc1 : acc0;
+        if (mode == 0) {
+            const int64_t n = (int64_t)r * Nc * Nc + (int64_t)i * Nc + j;
 #pragma unroll
-        for (int c = 0; c < KC; ++c)
-            if (c < Nch) o[c] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
+            for (int c = 0; c < KC; ++c)
+                if (c < Nch) out[(int64_t)c * Nx + n] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
+        } else {
+            const int64_t vox = ((int64_t)rl * Nc + i) * Nc + j;
+            float* o = out + vox * ld_out + col0;
+#pragma unroll
+            for (int c = 0; c < KC; ++c)
+                if (c < Nch) o[c] = ((c & 1) ? acc[c >> 1].y : acc[c >> 1].x) * scale;
+        }
     }
 }
 
@@ -233,19 +311,20 @@ cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* i
 template <int KC>
 static cudaError_t bp_k(const Geometry& g, const DeviceTables& t, const float* Q, int Nch, int s0,
                         int ns, int mode, float* out, int64_t ld_out, int64_t col0, cudaStream_t s) {
-    const int per_view = WMAX * bp_pitch(KC) * (int)sizeof(float);
-    int vchunk = std::min(std::min(g.Nv, 64), std::max(1, (96 * 1024) / per_view));
-    const size_t smem = (size_t)vchunk * per_view;
+    // views per chunk: two buffers of about 20 KB (KC <= 8: four blocks per SM) or 40 KB
+    // (KC = 16: two blocks per SM, 128 registers) each
+    const int per_view = BWMAX * bp_pitch(KC) * (int)sizeof(float);
+    const int vch = std::max(1, std::min(std::min(g.Nv, BVMAX), ((KC <= 8 ? 20 : 40) * 1024) / per_view));
+    const size_t smem = (size_t)2 * vch * per_view;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_backproject<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_backproject<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
     const int nchunk = (Nch + KC - 1) / KC;
-    dim3 grid((g.Nc + TILE - 1) / TILE, (g.Nc + TILE - 1) / TILE, ns * nchunk);
-    k_backproject<KC><<<grid, TILE * TILE, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode,
-                                                     out, ld_out, col0,
-                                                     (int64_t)g.Nr * g.Nc * g.Nc, vchunk);
+    dim3 grid((g.Nc + BTX - 1) / BTX, (g.Nc + BTY - 1) / BTY, ns * nchunk);
+    k_backproject<KC><<<grid, BTX * BTY / 2, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode, out,
+                                                       ld_out, col0, (int64_t)g.Nr * g.Nc * g.Nc, vch);
     return cudaGetLastError();
 }
 
@@ -254,9 +333,14 @@ cudaError_t backproject(const Geometry& g, const DeviceTables& t, const float* Q
                         cudaStream_t s) {
     if (ns <= 0) return cudaSuccess;
     switch (Kc) {
+        case 1: return bp_k<1>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+        case 2: return bp_k<2>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+        case 3: return bp_k<3>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
         case 4: return bp_k<4>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+        case 5: return bp_k<5>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+        case 6: return bp_k<6>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+        case 7: return bp_k<7>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
         case 8: return bp_k<8>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
-        case 12: return bp_k<12>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
         case 16: return bp_k<16>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
         default: return cudaErrorInvalidValue;
     }
