@@ -197,6 +197,16 @@ uint64_t hsnct_kernel_launches(hsnct_t h);
  * (both nullable).  Synchronous. */
 hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta);
 
+/* Diagnostics: stage timing of hsnct_fbp (bench.py's per-stage rooflines).
+ * hsnct_debug_fbp_timing(h, 1) makes every later hsnct_fbp call record CUDA events
+ * around its ramp-filter and backprojection launches (on the call's stream);
+ * hsnct_debug_fbp_timing(h, 0) stops it (synchronises the device).
+ * hsnct_debug_fbp_times waits for the last timed call and writes its two durations in
+ * milliseconds to the HOST array ms[2] = {ramp filter, backprojection};
+ * HSNCT_E_ARG when no timed call was made since timing was switched on. */
+hsnct_status hsnct_debug_fbp_timing(hsnct_t h, int on);
+hsnct_status hsnct_debug_fbp_times(hsnct_t h, float* ms);
+
 /* Static description of a status code; never NULL. */
 const char* hsnct_status_string(hsnct_status st);
 

@@ -29,6 +29,8 @@ struct hsnct_s {
     uint64_t launches = 0;
     uint64_t* trace = nullptr;        // diagnostics buffer (HSNCT_TRACE=1 at create)
     int trace_iters = 0;
+    cudaEvent_t fbp_ev[3] = {nullptr, nullptr, nullptr};  // stage timing of hsnct_fbp (diagnostics)
+    bool fbp_timed = false;                               // events of the last call are recorded
 };
 
 namespace {
@@ -187,8 +189,13 @@ hsnct_status run_fbp(hsnct_t h, const float* V, float* X, void* ws, cudaStream_t
     const Geometry& g = h->g;
     float* Q = static_cast<float*>(ws);
     const int kc = kc_of(g.K);
+    const bool timed = h->fbp_ev[0] != nullptr;
+    if (timed) CK(cudaEventRecord(h->fbp_ev[0], s), "fbp timing");
     CK(ramp_filter(g, h->t, V, g.K, g.K, 0, g.Nr, Q, kc, s), "fbp ramp filter");
+    if (timed) CK(cudaEventRecord(h->fbp_ev[1], s), "fbp timing");
     CK(backproject(g, h->t, Q, kc, g.K, 0, g.Nr, 0, X, 0, 0, s), "fbp backprojection");
+    if (timed) CK(cudaEventRecord(h->fbp_ev[2], s), "fbp timing");
+    h->fbp_timed = timed;
     h->launches += 2;
     return HSNCT_OK;
 }
@@ -353,6 +360,8 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.status);
     cudaFree(h->t.counter);
     cudaFree(h->trace);
+    for (cudaEvent_t e : h->fbp_ev)
+        if (e) cudaEventDestroy(e);
     if (h->status_host) cudaFreeHost(h->status_host);
     delete h;
 }
@@ -613,6 +622,35 @@ hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_ou
     if (!host) return fail(HSNCT_E_ARG, "debug_trace: host buffer is NULL");
     DeviceGuard guard(h->device);
     CK(cudaMemcpy(host, h->trace, m * sizeof(uint64_t), cudaMemcpyDeviceToHost), "debug_trace");
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_debug_fbp_timing(hsnct_t h, int on) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_fbp_timing: handle is NULL");
+    DeviceGuard guard(h->device);
+    if (on && !h->fbp_ev[0]) {
+        for (cudaEvent_t& e : h->fbp_ev) CK(cudaEventCreate(&e), "debug_fbp_timing");
+    } else if (!on && h->fbp_ev[0]) {
+        CK(cudaDeviceSynchronize(), "debug_fbp_timing");
+        for (cudaEvent_t& e : h->fbp_ev) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
+    }
+    h->fbp_timed = false;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_debug_fbp_times(hsnct_t h, float* ms) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_fbp_times: handle is NULL");
+    if (!ms) return fail(HSNCT_E_ARG, "debug_fbp_times: ms is NULL");
+    if (!h->fbp_timed) return fail(HSNCT_E_ARG, "debug_fbp_times: no timed hsnct_fbp call");
+    DeviceGuard guard(h->device);
+    CK(cudaEventSynchronize(h->fbp_ev[2]), "debug_fbp_times");
+    CK(cudaEventElapsedTime(&ms[0], h->fbp_ev[0], h->fbp_ev[1]), "debug_fbp_times");
+    CK(cudaEventElapsedTime(&ms[1], h->fbp_ev[1], h->fbp_ev[2]), "debug_fbp_times");
     return HSNCT_OK;
 }
 

@@ -15,6 +15,7 @@
 // X[k][r][i][j]) and the DHR baseline (channels = a chunk of wavelength bins,
 // output Xh[voxel][bin]).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -134,6 +135,154 @@ __global__ void __launch_bounds__(RT) k_ramp(const float* __restrict__ in, int64
 }
 
 // cp.async of VEC floats with zero fill (src_bytes = 0 -> zeros); 4/8/16-byte forms
+// ---------------------------------------------------------------------------------------
+// Ramp filter for P = 32 B <= 1024 (B in {4, 8, 16, 32}): the same FFT convolution as k_ramp,
+// computed as a four-step FFT whose short DFTs run in registers.  With n = 32 j + l and
+// k = k1 + B k2:
+//   pass 1  thread (pair, l):  B-point DFT over j of x[32 j + l] (j >= B/2 is the zero
+//           padding, P >= 2 N_c), times W_P^(l k1)                      -> T[k1][l]
+//   pass 2  thread (pair, k1): 32-point DFT over l -> X[k1 + B k2]; times H^[k1 + B k2];
+//           32-point inverse DFT over k2; times W_P^(-l k1)              -> T[k1][l]
+//   pass 3  thread (pair, l):  B-point inverse DFT over k1 -> q[l + 32 j], kept for < N_c.
+// Shared memory only between the passes (rows of 33 complex values: conflict-free).
+
+// cos(k pi / 16) for any integer k (exact table of the first octant)
+__host__ __device__ constexpr double cos16(int k) {
+    constexpr double C[9] = {1.0,
+                             0.98078528040323044913,
+                             0.92387953251128675613,
+                             0.83146961230254523708,
+                             0.70710678118654752440,
+                             0.55557023301960222474,
+                             0.38268343236508977173,
+                             0.19509032201612826785,
+                             0.0};
+    k = ((k % 32) + 32) % 32;
+    return k <= 8 ? C[k] : (k <= 16 ? -C[16 - k] : (k <= 24 ? -C[k - 16] : C[32 - k]));
+}
+// W_N^k = exp(-2 pi i k / N) (INV: conjugate), N | 32
+template <int N, bool INV>
+__device__ __forceinline__ float2 wn(int k) {
+    const int q = k * (32 / N);  // in units of pi / 16: 2 pi k / N = q pi / 16
+    const float c = (float)cos16(q), sn = (float)cos16(q - 8);  // sin x = cos(x - pi/2)
+    return make_float2(c, INV ? sn : -sn);
+}
+__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
+__host__ __device__ constexpr int brevc(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b) r |= ((i >> b) & 1) << (bits - 1 - b);
+    return r;
+}
+// In-register radix-2 DIT DFT of length N (natural order in and out), unnormalised.
+template <int N, bool INV>
+__device__ __forceinline__ void dft_reg(float2 (&x)[N]) {
+    constexpr int L = ilog2c(N);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const int j = brevc(i, L);
+        if (j > i) {
+            const float2 t = x[i];
+            x[i] = x[j];
+            x[j] = t;
+        }
+    }
+#pragma unroll
+    for (int m = 1; m < N; m <<= 1) {
+#pragma unroll
+        for (int i0 = 0; i0 < N; i0 += 2 * m) {
+#pragma unroll
+            for (int j = 0; j < m; ++j) {
+                const float2 tw = wn<N, INV>(j * (N / (2 * m)));
+                const float2 a = x[i0 + j], b0 = x[i0 + j + m];
+                const float2 b = (j == 0) ? b0 : cmul(tw, b0);
+                x[i0 + j] = make_float2(a.x + b.x, a.y + b.y);
+                x[i0 + j + m] = make_float2(a.x - b.x, a.y - b.y);
+            }
+        }
+    }
+}
+// W_P^m from the [P/2] table (m in [0, P))
+__device__ __forceinline__ float2 twp(const float2* __restrict__ tw, int m, int half) {
+    const float2 w = __ldg(tw + (m < half ? m : m - half));
+    return m < half ? w : make_float2(-w.x, -w.y);
+}
+
+template <int B>
+__global__ void __launch_bounds__(256, 2) k_ramp_reg(const float* __restrict__ in, int64_t ld_in, int NchAll,
+                                                    int Nv, int Nr, int Nc, int s0, int ns,
+                                                    const float* __restrict__ Hhat,
+                                                    const float2* __restrict__ tw, float* __restrict__ Q,
+                                                    int Kc) {
+    constexpr int P = 32 * B, RS = 33;  // row stride of T (complex)
+    extern __shared__ float2 T[];       // [npair][B][RS]
+    const int v = blockIdx.x, rl = blockIdx.y % ns, chunk = blockIdx.y / ns, r = s0 + rl;
+    in += (int64_t)chunk * Kc;
+    const int Nch = min(Kc, NchAll - chunk * Kc);
+    const int npair = (Nch + 1) >> 1;
+    const int tid = threadIdx.x;
+    const int64_t row0 = ((int64_t)v * Nr + r) * Nc;
+    // ---- pass 1
+    if (tid < 32 * npair) {
+        const int pr = tid >> 5, l = tid & 31, ch = 2 * pr;
+        float2 x[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            x[j] = make_float2(0.f, 0.f);
+            const int c = 32 * j + l;
+            if (j < B / 2 && c < Nc) {
+                const float* src = in + (row0 + c) * ld_in + ch;
+                x[j].x = __ldg(src);
+                if (ch + 1 < Nch) x[j].y = __ldg(src + 1);
+            }
+        }
+        dft_reg<B, false>(x);
+        float2* t = T + (pr * B) * RS + l;
+#pragma unroll
+        for (int k1 = 0; k1 < B; ++k1) t[k1 * RS] = k1 == 0 ? x[0] : cmul(twp(tw, l * k1, P / 2), x[k1]);
+    }
+    __syncthreads();
+    // ---- pass 2
+    if (tid < B * npair) {
+        const int pr = tid / B, k1 = tid - (tid / B) * B;
+        float2* t = T + (pr * B + k1) * RS;
+        float2 z[32];
+#pragma unroll
+        for (int l = 0; l < 32; ++l) z[l] = t[l];
+        dft_reg<32, false>(z);
+#pragma unroll
+        for (int k2 = 0; k2 < 32; ++k2) {
+            const float h = __ldg(Hhat + k1 + B * k2);
+            z[k2].x *= h;
+            z[k2].y *= h;
+        }
+        dft_reg<32, true>(z);
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            const float2 w = twp(tw, l * k1, P / 2);
+            t[l] = k1 == 0 ? z[l] : cmul(make_float2(w.x, -w.y), z[l]);
+        }
+    }
+    __syncthreads();
+    // ---- pass 3, store q[c], c < Nc: Q[chunk][rl][v][c][Kc]
+    if (tid < 32 * npair) {
+        const int pr = tid >> 5, l = tid & 31, ch = 2 * pr;
+        const float2* t = T + (pr * B) * RS + l;
+        float2 x[B];
+#pragma unroll
+        for (int k1 = 0; k1 < B; ++k1) x[k1] = t[k1 * RS];
+        dft_reg<B, true>(x);
+        float* dst = Q + ((((int64_t)chunk * ns + rl) * Nv + v) * Nc) * Kc;
+#pragma unroll
+        for (int j = 0; j < B / 2; ++j) {
+            const int c = 32 * j + l;
+            if (c < Nc) {
+                dst[(int64_t)c * Kc + ch] = x[j].x;
+                if (ch + 1 < Kc) dst[(int64_t)c * Kc + ch + 1] = ch + 1 < Nch ? x[j].y : 0.f;
+            }
+        }
+    }
+}
+
 template <int VEC>
 __device__ __forceinline__ void cp_async_zfill(float* dst, const float* src, bool ok) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -291,9 +440,35 @@ __global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
 
 }  // namespace
 
+template <int B>
+static cudaError_t ramp_reg(const Geometry& g, const DeviceTables& t, const float* in, int64_t ld_in, int Nch,
+                            int s0, int ns, float* Q, int Kc, cudaStream_t s) {
+    const int npair = (std::min(Nch, Kc) + 1) / 2;
+    const size_t smem = (size_t)npair * B * 33 * sizeof(float2);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ramp_reg<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+    }
+    const int nchunk = (Nch + Kc - 1) / Kc;
+    dim3 grid(g.Nv, ns * nchunk);
+    k_ramp_reg<B><<<grid, 32 * npair, smem, s>>>(in, ld_in, Nch, g.Nv, g.Nr, g.Nc, s0, ns, t.Hhat, t.twiddle, Q,
+                                                Kc);
+    return cudaGetLastError();
+}
+
 cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* in, int64_t ld_in,
                         int Nch, int s0, int ns, float* Q, int Kc, cudaStream_t s) {
     if (ns <= 0) return cudaSuccess;
+    if (Kc <= 16 && getenv("HSNCT_RAMP_SMEM") == nullptr) {  // register four-step FFT for P <= 1024
+        switch (g.P) {
+            case 128: return ramp_reg<4>(g, t, in, ld_in, Nch, s0, ns, Q, Kc, s);
+            case 256: return ramp_reg<8>(g, t, in, ld_in, Nch, s0, ns, Q, Kc, s);
+            case 512: return ramp_reg<16>(g, t, in, ld_in, Nch, s0, ns, Q, Kc, s);
+            case 1024: return ramp_reg<32>(g, t, in, ld_in, Nch, s0, ns, Q, Kc, s);
+            default: break;
+        }
+    }
     const int npair = (std::min(Nch, Kc) + 1) / 2;
     const size_t smem = (size_t)npair * g.P * sizeof(float2);
     static bool attr = false;

@@ -79,6 +79,10 @@ def lib():
             L.hsnct_fmd_spectra.restype = i32
             L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
             L.hsnct_debug_trace.restype = i32
+            L.hsnct_debug_fbp_timing.argtypes = [vp, ctypes.c_int]
+            L.hsnct_debug_fbp_timing.restype = i32
+            L.hsnct_debug_fbp_times.argtypes = [vp, vp]
+            L.hsnct_debug_fbp_times.restype = i32
             L.hsnct_abi_version.argtypes = []
             L.hsnct_abi_version.restype = i32
             _lib = L
@@ -278,6 +282,16 @@ class Hsnct:
         self._dev(Dm, "Dm", (n_mat, self.Nk))
         _check(lib().hsnct_fmd_spectra(self._h, _ptr(D), _ptr(T), int(n_mat), _ptr(Dm), _stream(stream, self.device)))
         return Dm
+
+    def debug_fbp_timing(self, on: bool):
+        """Record CUDA events around the ramp filter and backprojection of later fbp calls."""
+        _check(lib().hsnct_debug_fbp_timing(self._h, 1 if on else 0))
+
+    def debug_fbp_times(self):
+        """(ramp filter ms, backprojection ms) of the last timed fbp call (waits for it)."""
+        ms = (ctypes.c_float * 2)()
+        _check(lib().hsnct_debug_fbp_times(self._h, ctypes.cast(ms, ctypes.c_void_p)))
+        return float(ms[0]), float(ms[1])
 
     def debug_trace(self):
         """Per-iteration, per-CTA phase stamps of the last persistent decompose (ns), as a

@@ -177,6 +177,23 @@ def test_fbp_parity(H, cfg):
     assert rel(X, Xo) <= 1e-4, rel(X, Xo)
 
 
+def test_fbp_stage_timing(H):
+    """hsnct_debug_fbp_timing/_times: events around the two launches, same result."""
+    from paper_2410_22500_b200.hsnct import HsnctError
+    cfg = sd.custom(idx=22, Nc=64, Nv=30, Nr=2, Nk=8, K=6)
+    V = torch.rand((cfg.Np, cfg.K), generator=torch.Generator().manual_seed(3)).to(DEV)
+    h = H(cfg)
+    X0 = h.fbp(V)
+    h.debug_fbp_timing(True)
+    X1 = h.fbp(V)
+    ramp_ms, bp_ms = h.debug_fbp_times()
+    h.debug_fbp_timing(False)
+    assert ramp_ms > 0 and bp_ms > 0
+    assert torch.equal(X0, X1)
+    with pytest.raises(HsnctError):
+        h.debug_fbp_times()
+
+
 def test_fbp_custom_angles(H):
     cfg = sd.custom(idx=14, Nc=40, Nv=17, Nk=6, K=3)
     ang = np.sort(np.random.default_rng(2).uniform(0, math.pi, cfg.Nv))
