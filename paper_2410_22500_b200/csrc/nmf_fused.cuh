@@ -719,6 +719,15 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
         stamp(it, 1);
         grid_sync(A.bar, epoch);
         stamp(it, 2);
+        // <V_new, A> for the objective (last CTA): read between the two barriers -- after the
+        // second one, CTAs already in the next pass overwrite their vpart
+        const bool objcta = c == nC - 1 && (A.obj || it == 0);
+        double va = 0.0;
+        if (objcta) {
+            double v0 = 0.0;
+            for (int i = tid; i < nC; i += NTH) v0 += __ldcg(A.vpart + 2 * i);
+            va = block_sum_all(v0, red);
+        }
         // ---- H (KK outputs) and the B slice (K x nsl outputs) over the nC partials
         {
             const int nB = K * nsl, nout = KK + nB;
@@ -827,15 +836,11 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
             __syncthreads();
         }
         stamp(it, 7);
-        if (c == nC - 1 && (A.obj || it == 0)) {  // the objective trace (and the Y+ = 0 check)
-            double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-            for (int i = tid; i < nC; i += NTH) {
-                v0 += __ldcg(A.vpart + 2 * i);
-                v2 += __ldcg(A.dpart + i);
-            }
+        if (objcta) {  // the objective trace (and the Y+ = 0 check)
+            double v1 = 0.0, v2 = 0.0;
+            for (int i = tid; i < nC; i += NTH) v2 += __ldcg(A.dpart + i);
             if (it == 0)
                 for (int i = tid; i < A.nby; i += NTH) v1 += __ldcg(A.ypart + i);
-            const double va = block_sum_all(v0, red);
             const double ysq_new = block_sum_all(v1, red);
             const double bdot = block_sum_all(v2, red);
             if (tid == 0) {
@@ -855,6 +860,7 @@ __global__ void __launch_bounds__(NGRP * TG, 1) k_nmf_persist(PersistArgs A) {
                 }
             }
         }
+        __syncthreads();  // the objective (thread 0) has read Gold; K*K > 32 spans several warps
         for (int o = tid; o < KK; o += NTH) Gold[o] = Gnew[o];
         __syncthreads();
         stamp(it, 4);

@@ -494,6 +494,14 @@ __global__ void __launch_bounds__(MTHREADS, 1) k_nmf_mma(MmaArgs A) {
         stamp(it, 1);
         grid_sync(A.bar, epoch);
         stamp(it, 2);
+        // <V_new, A> for the objective (last CTA), read before the second barrier (after it,
+        // CTAs already in the next pass overwrite their vpart)
+        double va = 0.0;
+        if (c == nC - 1) {
+            double v0 = 0.0;
+            for (int i = tid; i < nC; i += MTHREADS) v0 += __ldcg(A.vpart + 2 * i);
+            va = block_sum_all(v0, sh.dred);
+        }
         // ============================== D update ==================================
         {
             const int nB = K * nsl, nout = KK + nB;
@@ -583,14 +591,10 @@ __global__ void __launch_bounds__(MTHREADS, 1) k_nmf_mma(MmaArgs A) {
             __syncthreads();
         }
         if (c == nC - 1) {
-            double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-            for (int i = tid; i < nC; i += MTHREADS) {
-                v0 += __ldcg(A.vpart + 2 * i);
-                v2 += __ldcg(A.dpart + i);
-            }
+            double v1 = 0.0, v2 = 0.0;
+            for (int i = tid; i < nC; i += MTHREADS) v2 += __ldcg(A.dpart + i);
             if (it == 0)
                 for (int i = tid; i < A.nby; i += MTHREADS) v1 += __ldcg(A.ypart + i);
-            const double va = block_sum_all(v0, sh.dred);
             const double ysq_new = block_sum_all(v1, sh.dred);
             const double bdot = block_sum_all(v2, sh.dred);
             if (tid == 0) {
@@ -610,6 +614,7 @@ __global__ void __launch_bounds__(MTHREADS, 1) k_nmf_mma(MmaArgs A) {
                 }
             }
         }
+        __syncthreads();  // the objective (thread 0) has read Gold; K*K > 32 spans several warps
         for (int o = tid; o < KK; o += MTHREADS) sh.Gold[o] = sh.Gnew[o];
         __syncthreads();
         stamp(it, 4);

@@ -48,6 +48,10 @@ def padded(Y, ld, fill=float("nan")):
     (sd.custom(idx=7, Nc=20, Nv=13, Nk=203, K=5, M=4), 40),     # ragged N_p, N_k % 4 != 0
     (sd.custom(idx=8, Nc=17, Nv=9, Nk=37, K=1, M=2), 30),       # K = 1
     (sd.custom(idx=9, Nc=24, Nv=10, Nr=3, Nk=64, K=16, M=5), 25),  # K = 16, several slices
+    # three groups with a row-split last lambda slot (17 pairs past 3 x 128), ragged N_k
+    (sd.custom(idx=23, Nc=24, Nv=11, Nr=1, Nk=801, K=6, M=6), 20),
+    # K*K = 64 > 32: the objective reads G_old across several warps
+    (sd.custom(idx=24, Nc=24, Nv=11, Nr=1, Nk=200, K=8, M=4), 10),
 ])
 def test_nmf_parity(H, cfg, n_iter):
     pr = sd.make_problem(cfg)
