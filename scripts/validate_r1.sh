@@ -1,0 +1,7 @@
+# round-1 validation: full GPU suite, smoke, default bench (+ CPU baseline), reference arm,
+# every config at its full iteration count
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "default rc=$?"
+timeout 900 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+bash scripts/bench_all.sh
