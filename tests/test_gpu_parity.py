@@ -170,6 +170,8 @@ def test_nmf_zero_iterations_noop(H):
     sd.custom(idx=11, Nc=63, Nv=37, Nr=2, Nk=10, K=5),
     sd.custom(idx=12, Nc=100, Nv=45, Nr=1, Nk=20, K=16),
     sd.custom(idx=13, Nc=33, Nv=8, Nr=3, Nk=4, K=1),
+    sd.custom(idx=26, Nc=300, Nv=9, Nr=2, Nk=6, K=5),   # P = 1024 (32 x 32 four-step FFT), KC = 5
+    sd.custom(idx=27, Nc=130, Nv=12, Nr=1, Nk=8, K=7),  # P = 512, KC = 7 (scalar window loads)
 ])
 def test_fbp_parity(H, cfg):
     g = torch.Generator().manual_seed(cfg.idx)
@@ -179,6 +181,23 @@ def test_fbp_parity(H, cfg):
     torch.cuda.synchronize()
     Xo = oracle.fbp(V.numpy(), cfg.Nv, cfg.Nr, cfg.Nc)
     assert rel(X, Xo) <= 1e-4, rel(X, Xo)
+
+
+def test_fbp_and_dhr_large_detector(H):
+    """N_c = 600 -> P = 2048: the shared-memory radix-2 ramp filter (P > 1024) and, for DHR,
+    8-bin channel chunks (backprojection KC = 8)."""
+    cfg = sd.custom(idx=25, Nc=600, Nv=7, Nr=1, Nk=11, K=3)
+    g = torch.Generator().manual_seed(8)
+    V = torch.rand((cfg.Np, cfg.K), generator=g)
+    h = H(cfg)
+    X = h.fbp(V.to(DEV))
+    Y = torch.rand((cfg.Np, cfg.Nk), generator=g) - 0.1
+    Xh = h.dhr(padded(Y, 12), 0, 1, 1, 9)
+    torch.cuda.synchronize()
+    Xo = oracle.fbp(V.numpy(), cfg.Nv, cfg.Nr, cfg.Nc)
+    assert rel(X, Xo) <= 1e-4, rel(X, Xo)
+    Xho = oracle.dhr(Y.numpy(), cfg.Nv, cfg.Nr, cfg.Nc, slice0=0, n_slices=1, bin0=1, n_bins=9)
+    assert rel(Xh, Xho) <= 1e-4, rel(Xh, Xho)
 
 
 def test_fbp_stage_timing(H):
