@@ -30,7 +30,10 @@
     } while (0)
 
 constexpr int TM = 128;      // rows per tile (UMMA M)
-constexpr int NN = 16;       // UMMA N (K components padded)
+#ifndef NNV
+#define NNV 16
+#endif
+constexpr int NN = NNV;       // UMMA N (K components padded)
 constexpr int CL = 64;       // lambda per chunk
 constexpr int NST = 3;       // chunk stages
 constexpr int CHB = TM * CL * 2;  // bytes per hi (or lo) chunk = 16 KB
@@ -84,7 +87,7 @@ __device__ __forceinline__ void commit(uint64_t* b) {
 
 // Yc: [tiles][chunks][2][CHB] (hi, lo), core-matrix order within a chunk:
 //     ((pb * 8 + lb) * 8 + r) * 8 + l  for row 8 pb + r, lambda 8 lb + l of the chunk
-// Dc: [2][NK/8][2][8][8] (hi, lo): core matrix (lb, nb) at (lb * 2 + nb) * 64 halves
+// Dc: [2][NK/8][NN/8][8][8] (hi, lo): core matrix (lb, nb) at (lb * NN/8 + nb) * 64 halves
 __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc, const __half* __restrict__ Dc,
                                                  float* __restrict__ Aout, int ntiles, int nchunk) {
     extern __shared__ __align__(1024) uint8_t sm[];
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {  // TMEM: 2 accumulators x 16 columns
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(su32(&tbase)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -159,9 +162,10 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
                     for (int k = 0; k < CL / 16; ++k) {
                         // A: core (pb, lb) at (pb * 8 + lb) * 128 B: K step (lb) 128 B, M step (pb) 1024 B
                         const uint64_t aH = sdesc(ah + k * 256, 128, 1024), aL = sdesc(al + k * 256, 128, 1024);
-                        // B: core (lb, nb) at (lb * 2 + nb) * 128 B: K step 256 B, N step 128 B
-                        const uint32_t boff = (uint32_t)(c * (CL / 8) + 2 * k) * 256;
-                        const uint64_t bH = sdesc(dh + boff, 256, 128), bL = sdesc(dl + boff, 256, 128);
+                        // B: core (lb, nb) at (lb * NB + nb) * 128 B: K step NB * 128 B, N step 128 B
+                        constexpr uint32_t NB = NN / 8;
+                        const uint32_t boff = (uint32_t)(c * (CL / 8) + 2 * k) * NB * 128;
+                        const uint64_t bH = sdesc(dh + boff, NB * 128, 128), bL = sdesc(dl + boff, NB * 128, 128);
                         const uint32_t first = (c == 0 && k == 0) ? 0u : 1u;
                         mma(td, aH, bH, first);
                         mma(td, aH, bL, 1u);
@@ -196,13 +200,13 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
             const int t = blockIdx.x + m * gridDim.x;
             float4* o = reinterpret_cast<float4*>(Aout + ((size_t)t * TM + 32 * q + lane) * NN);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < NN / 4; ++j)
                 o[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]), __uint_as_float(v[4 * j + 2]),
                                    __uint_as_float(v[4 * j + 3]));
         }
     }
     __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
 int main(int argc, char** argv) {
@@ -246,7 +250,7 @@ int main(int argc, char** argv) {
             const float d = D[(size_t)n * NK + l];
             const __half hi = __float2half_rn(d);
             const __half lo = __float2half_rn(d - __half2float(hi));
-            const size_t off = (((size_t)(l >> 3) * 2 + (n >> 3)) * 8 + (n & 7)) * 8 + (l & 7);
+            const size_t off = (((size_t)(l >> 3) * (NN / 8) + (n >> 3)) * 8 + (n & 7)) * 8 + (l & 7);
             Dc[off] = hi;
             Dc[(size_t)NK * NN + off] = lo;
         }
