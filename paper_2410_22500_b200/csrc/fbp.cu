@@ -192,13 +192,35 @@ __device__ __forceinline__ void dft_reg(float2 (&x)[N]) {
         for (int i0 = 0; i0 < N; i0 += 2 * m) {
 #pragma unroll
             for (int j = 0; j < m; ++j) {
-                const float2 tw = wn<N, INV>(j * (N / (2 * m)));
+                const int q = j * (N / (2 * m));  // twiddle W_N^q (compile-time)
+                const float2 tw = wn<N, INV>(q);
                 const float2 a = x[i0 + j], b0 = x[i0 + j + m];
-                const float2 b = (j == 0) ? b0 : cmul(tw, b0);
+                // W = 1 and W = -i (+i inverse) are exact swaps / negations
+                const float2 b = (q == 0)       ? b0
+                                 : (4 * q == N) ? (INV ? make_float2(-b0.y, b0.x) : make_float2(b0.y, -b0.x))
+                                                : cmul(tw, b0);
                 x[i0 + j] = make_float2(a.x + b.x, a.y + b.y);
                 x[i0 + j + m] = make_float2(a.x - b.x, a.y - b.y);
             }
         }
+    }
+}
+// Forward DFT of length N whose inputs x[N/2..N) are zero (the zero padding of pass 1): the
+// first decimation-in-frequency split leaves two N/2-point DFTs, of x and of x W_N^j.
+template <int N>
+__device__ __forceinline__ void dft_reg_halfzero(float2 (&x)[N]) {
+    float2 e[N / 2], o[N / 2];
+#pragma unroll
+    for (int j = 0; j < N / 2; ++j) {
+        e[j] = x[j];
+        o[j] = j == 0 ? x[0] : (4 * j == N ? make_float2(x[j].y, -x[j].x) : cmul(wn<N, false>(j), x[j]));
+    }
+    dft_reg<N / 2, false>(e);
+    dft_reg<N / 2, false>(o);
+#pragma unroll
+    for (int k = 0; k < N / 2; ++k) {
+        x[2 * k] = e[k];
+        x[2 * k + 1] = o[k];
     }
 }
 // W_P^m from the [P/2] table (m in [0, P))
@@ -235,7 +257,7 @@ __global__ void __launch_bounds__(256, 2) k_ramp_reg(const float* __restrict__ i
                 if (ch + 1 < Nch) x[j].y = __ldg(src + 1);
             }
         }
-        dft_reg<B, false>(x);
+        dft_reg_halfzero<B>(x);
         float2* t = T + (pr * B) * RS + l;
 #pragma unroll
         for (int k1 = 0; k1 < B; ++k1) t[k1 * RS] = k1 == 0 ? x[0] : cmul(twp(tw, l * k1, P / 2), x[k1]);
