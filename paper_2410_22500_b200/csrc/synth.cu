@@ -98,33 +98,41 @@ __global__ void __launch_bounds__(ST) k_synth_v(const float* __restrict__ X, con
     const bool full = 4 * q + 3 < nb;
     const int64_t nchunk = (nn + 31) >> 5;
     const int64_t wstride = (int64_t)gridDim.x * (ST / 32);
+    // this warp's X chunk, k-major, so that one broadcast LDS.128 serves four voxels
+    __shared__ __align__(16) float xs[ST / 32][K][32];
     for (int64_t ch = (int64_t)blockIdx.x * (ST / 32) + warp; ch < nchunk; ch += wstride) {
         const int64_t nb0 = ch << 5;
         const int cnt = (int)min((int64_t)32, nn - nb0);
-        float xk[K];
+        __syncwarp();  // the previous chunk's reads of xs are done
 #pragma unroll
-        for (int k = 0; k < K; ++k) xk[k] = lane < cnt ? __ldg(X + (int64_t)k * Nx + n0 + nb0 + lane) : 0.f;
+        for (int k = 0; k < K; ++k) xs[warp][k][lane] = lane < cnt ? __ldg(X + (int64_t)k * Nx + n0 + nb0 + lane) : 0.f;
+        __syncwarp();
         float* dst = Xh + nb0 * ld + 4 * q;
-#pragma unroll 4
-        for (int i = 0; i < cnt; ++i) {
-            float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
+        for (int i = 0; i < cnt; i += 4) {
+            float4 xv[K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const float x = __shfl_sync(0xffffffffu, xk[k], i);
-                o01 = ffma2s(x, make_float2(d[k].x, d[k].y), o01);
-                o23 = ffma2s(x, make_float2(d[k].z, d[k].w), o23);
-            }
-            if (act) {
-                if (full) {
-                    __stcs(reinterpret_cast<float4*>(dst), make_float4(o01.x, o01.y, o23.x, o23.y));
-                } else {
-                    const int valid = nb - 4 * q;
-                    __stcs(dst, o01.x);
-                    if (valid > 1) __stcs(dst + 1, o01.y);
-                    if (valid > 2) __stcs(dst + 2, o23.x);
+            for (int k = 0; k < K; ++k) xv[k] = *reinterpret_cast<const float4*>(&xs[warp][k][i]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                float2 o01 = make_float2(0.f, 0.f), o23 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const float x = j == 0 ? xv[k].x : (j == 1 ? xv[k].y : (j == 2 ? xv[k].z : xv[k].w));
+                    o01 = ffma2s(x, make_float2(d[k].x, d[k].y), o01);
+                    o23 = ffma2s(x, make_float2(d[k].z, d[k].w), o23);
                 }
+                if (act && i + j < cnt) {
+                    if (full) {
+                        __stcs(reinterpret_cast<float4*>(dst), make_float4(o01.x, o01.y, o23.x, o23.y));
+                    } else {
+                        const int valid = nb - 4 * q;
+                        __stcs(dst, o01.x);
+                        if (valid > 1) __stcs(dst + 1, o01.y);
+                        if (valid > 2) __stcs(dst + 2, o23.x);
+                    }
+                }
+                dst += ld;
             }
-            dst += ld;
         }
     }
 }
