@@ -31,7 +31,11 @@ constexpr int BVMAX = 64;          // views per staged chunk (upper bound)
 // floats per staged detector sample: KC, plus 4 when KC is a multiple of 8 (an odd number
 // of 16-byte chunks per sample spreads a quarter-warp's LDS.128 over all bank groups; the
 // other widths are conflict-free as they are for neighbouring samples)
-__host__ __device__ constexpr int bp_pitch(int KC) { return KC % 8 == 0 ? KC + 4 : KC; }
+// K = 3 and 5 are padded to 4 and 6 (one LDS.128 / three LDS.64 per sample instead of 3 / 5
+// scalar loads; the pad channel is never stored)
+__host__ __device__ constexpr int bp_pitch(int KC) {
+    return KC % 8 == 0 ? KC + 4 : (KC == 3 || KC == 5 ? KC + 1 : KC);
+}
 
 __device__ __forceinline__ unsigned bitrev(unsigned x, int logP) { return __brev(x) >> (32 - logP); }
 
@@ -332,8 +336,9 @@ __global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
     const float* __restrict__ sin_t, int mode, float* __restrict__ out, int64_t ld_out, int64_t col0,
     int64_t Nx, int vch) {
     constexpr int NT = BTX * BTY / 2;
-    constexpr int VEC = KC % 4 == 0 ? 4 : (KC % 2 == 0 ? 2 : 1);  // floats per copy / per LDS
+    constexpr int VEC = KC % 4 == 0 ? 4 : (KC % 2 == 0 ? 2 : 1);  // floats per copy (global alignment)
     constexpr int SP = bp_pitch(KC);                               // floats per staged sample
+    constexpr int LV = SP % 4 == 0 ? 4 : (SP % 2 == 0 ? 2 : 1);    // floats per shared-memory load
     constexpr int WQ = BWMAX * KC;                                 // floats per view window in Q
     constexpr int WIN = BWMAX * SP;                                // ... and in shared memory
     extern __shared__ __align__(16) float Ws[];                    // [2][vch][WIN]
@@ -386,15 +391,15 @@ __global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
     // (1 - w) q[l] + w q[l + 1] into acc, KC channels from the window at p
     auto interp = [&](float2* acc, const float* p, float wt) {
         const float w1 = 1.f - wt;
-        float a[KC + 1], bq[KC + 1];
+        float a[SP + 1], bq[SP + 1];
 #pragma unroll
-        for (int c = 0; c < KC; c += VEC) {
-            if constexpr (VEC == 4) {
+        for (int c = 0; c < KC; c += LV) {
+            if constexpr (LV == 4) {
                 const float4 qa = *reinterpret_cast<const float4*>(p + c);
                 const float4 qb = *reinterpret_cast<const float4*>(p + SP + c);
                 a[c] = qa.x; a[c + 1] = qa.y; a[c + 2] = qa.z; a[c + 3] = qa.w;
                 bq[c] = qb.x; bq[c + 1] = qb.y; bq[c + 2] = qb.z; bq[c + 3] = qb.w;
-            } else if constexpr (VEC == 2) {
+            } else if constexpr (LV == 2) {
                 const float2 qa = *reinterpret_cast<const float2*>(p + c);
                 const float2 qb = *reinterpret_cast<const float2*>(p + SP + c);
                 a[c] = qa.x; a[c + 1] = qa.y;
