@@ -88,11 +88,11 @@ __device__ __forceinline__ void tr_step(float* v, int lane) {
         tr_step<O / 2, n>(v, lane);
     }
 }
-template <int N>
+template <int N, int O0 = 16>
 __device__ __forceinline__ int tr_base(int lane) {
     int b = 0, n = N;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
+    for (int o = O0; o; o >>= 1) {
         if (n % 2 == 0) {
             if (lane & o) b += n / 2;
             n /= 2;
@@ -212,6 +212,9 @@ struct Pass {
     // Three groups only: at four (128 registers) the branch measured slower than multiplying
     // zeros (C2 49.1 -> 50.0 us per iteration), at three it pays with the slot rotation.
     static constexpr bool SKIP = NGRP == 3;
+    // lane-dependent phase-1 row order, select-free first two steps of the transpose-reduce
+    // (three groups: C4 6.34 -> 6.22 ms; at four groups' 128 registers it spilled, C2 +7%)
+    static constexpr bool RSWAP = NGRP == 3;
 
     const float* __restrict__ Yp;
     int64_t Np;
@@ -299,6 +302,7 @@ struct Pass {
         for (int x = 0; x < (KK + 31) / 32; ++x) hacc[x] = 0.0;
         unsigned bad = 0;
         const unsigned fullb = smem_u32(&sh.full[g][0]), partb = smem_u32(&sh.part[g][0]);
+        const int rsw = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);  // phase-1 row swap (see the reduction)
         // running slot / mbarrier phase / first row of the group's current tile (no 64-bit
         // division or multiply per tile)
         int b = (int)(n0 % NBG);
@@ -355,7 +359,7 @@ struct Pass {
                 float2 yy[RG];
 #pragma unroll
                 for (int r = 0; r < RG; ++r)
-                    yy[r] = ok ? *reinterpret_cast<const float2*>(yb + (size_t)r * Nkp + 2 * TG * i)
+                    yy[r] = ok ? *reinterpret_cast<const float2*>(yb + (size_t)(RSWAP ? r ^ rsw : r) * Nkp + 2 * TG * i)
                                : make_float2(0.f, 0.f);
                 float dd[2 * KD];
 #pragma unroll
@@ -382,12 +386,28 @@ struct Pass {
             for (int r = 0; r < RG; ++r)
 #pragma unroll
                 for (int k = 0; k < K; ++k) part[r * K + k] = (k & 1) ? p2[r][k >> 1].y : p2[r][k >> 1].x;
-            tr_step<16, GK>(part, lane);
             const int par = (int)(ncount & 1);
-            if (((unsigned)lane & tr_bfly(GK)) == 0) {
-                const int base = tr_base<GK>(lane);
+            if constexpr (RSWAP) {
+                // local row r of this lane is tile row r ^ rsw, so the two row halvings (lane bits
+                // 16 and 8) need no select: every lane keeps its local rows 0 (,1) and sends the
+                // others; afterwards it holds the K partials of tile row rsw, reduced over k below
 #pragma unroll
-                for (int x = 0; x < tr_nout(GK); ++x) sh.red[g][par][wg][base + x] = part[x];
+                for (int j = 0; j < GK / 2; ++j) part[j] += __shfl_xor_sync(0xffffffffu, part[j + GK / 2], 16);
+#pragma unroll
+                for (int j = 0; j < K; ++j) part[j] += __shfl_xor_sync(0xffffffffu, part[j + K], 8);
+                tr_step<4, K>(part, lane);
+                if (((unsigned)lane & tr_bfly(K, 4)) == 0) {
+                    const int base = rsw * K + tr_base<K, 4>(lane);
+#pragma unroll
+                    for (int x = 0; x < tr_nout(K, 4); ++x) sh.red[g][par][wg][base + x] = part[x];
+                }
+            } else {
+                tr_step<16, GK>(part, lane);
+                if (((unsigned)lane & tr_bfly(GK)) == 0) {
+                    const int base = tr_base<GK>(lane);
+#pragma unroll
+                    for (int x = 0; x < tr_nout(GK); ++x) sh.red[g][par][wg][base + x] = part[x];
+                }
             }
         };
         // ---- V update of the tile (every warp redundantly, lane s -> (r, k)) once the group's
