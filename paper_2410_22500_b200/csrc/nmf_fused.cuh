@@ -215,6 +215,8 @@ struct Pass {
     // lane-dependent phase-1 row order, select-free first two steps of the transpose-reduce
     // (three groups: C4 6.34 -> 6.22 ms; at four groups' 128 registers it spilled, C2 +7%)
     static constexpr bool RSWAP = NGRP == 3;
+    // four groups: only the first halving select-free (C2 48.3 -> 47.5 us; both halvings spilled)
+    static constexpr bool RSWAP1 = NGRP == 4;
 
     const float* __restrict__ Yp;
     int64_t Np;
@@ -359,7 +361,7 @@ struct Pass {
                 float2 yy[RG];
 #pragma unroll
                 for (int r = 0; r < RG; ++r)
-                    yy[r] = ok ? *reinterpret_cast<const float2*>(yb + (size_t)(RSWAP ? r ^ rsw : r) * Nkp + 2 * TG * i)
+                    yy[r] = ok ? *reinterpret_cast<const float2*>(yb + (size_t)(RSWAP ? r ^ rsw : (RSWAP1 ? r ^ (rsw & 2) : r)) * Nkp + 2 * TG * i)
                                : make_float2(0.f, 0.f);
                 float dd[2 * KD];
 #pragma unroll
@@ -400,6 +402,15 @@ struct Pass {
                     const int base = rsw * K + tr_base<K, 4>(lane);
 #pragma unroll
                     for (int x = 0; x < tr_nout(K, 4); ++x) sh.red[g][par][wg][base + x] = part[x];
+                }
+            } else if constexpr (RSWAP1) {
+#pragma unroll
+                for (int j = 0; j < GK / 2; ++j) part[j] += __shfl_xor_sync(0xffffffffu, part[j + GK / 2], 16);
+                tr_step<8, GK / 2>(part, lane);
+                if (((unsigned)lane & tr_bfly(GK / 2, 8)) == 0) {
+                    const int base = (rsw & 2) * K + tr_base<GK / 2, 8>(lane);
+#pragma unroll
+                    for (int x = 0; x < tr_nout(GK / 2, 8); ++x) sh.red[g][par][wg][base + x] = part[x];
                 }
             } else {
                 tr_step<16, GK>(part, lane);
