@@ -36,7 +36,7 @@ UNIT = "voxel*lambda/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, help="BASELINE.json configs[i-1]")
     ap.add_argument("--impl", default="hsnct", choices=["hsnct", "reference"])
@@ -91,8 +91,14 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a moment to start: wait for its first sample so that the timed
+            # region (which starts when this returns) is sampled from its beginning
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+        self.k0 = len(self.lines)  # samples from here on fall inside the timed region
         return self
 
     def _read(self):
@@ -101,6 +107,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            t0 = time.perf_counter()  # a very short timed region: take the next sample too
+            while len(self.lines) <= self.k0 and time.perf_counter() - t0 < 0.1:
+                time.sleep(0.002)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -110,7 +119,7 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "k0", 0):]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 6:
                 continue
