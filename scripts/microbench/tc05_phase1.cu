@@ -85,6 +85,19 @@ __device__ __forceinline__ void commit(uint64_t* b) {
                  : "memory");
 }
 
+// NPASS = 2 streams every tile twice, the second stream one tile later (P1(0), P1(1), P2(0),
+// P1(2), P2(1), ...), into a discarded accumulator: the L2 re-read a phase 2 would need.
+#ifndef NPASS
+#define NPASS 1
+#endif
+__device__ __forceinline__ void seq(int u, int mine, int& m, int& second) {
+    if (NPASS == 1) { m = u; second = 0; return; }
+    if (u == 0) { m = 0; second = 0; return; }
+    if (u & 1) {
+        if ((u + 1) / 2 < mine) { m = (u + 1) / 2; second = 0; }
+        else { m = mine - 1; second = 1; }
+    } else { m = u / 2 - 1; second = 1; }
+}
 // Yc: [tiles][chunks][2][CHB] (hi, lo), core-matrix order within a chunk:
 //     ((pb * 8 + lb) * 8 + r) * 8 + l  for row 8 pb + r, lambda 8 lb + l of the chunk
 // Dc: [2][NK/8][NN/8][8][8] (hi, lo): core matrix (lb, nb) at (lb * NN/8 + nb) * 64 halves
@@ -129,7 +142,9 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
             bulk(Dl, Dc + dbytes / 2, dbytes, &dbar);
             int s = 0;
             unsigned ph = 0;
-            for (int m = 0; m < mine; ++m) {
+            for (int u = 0; u < NPASS * mine; ++u) {
+                int m, second;
+                seq(u, mine, m, second);
                 const int t = blockIdx.x + m * gridDim.x;
                 for (int c = 0; c < nchunk; ++c) {
                     mb_wait(&empty[s], ph ^ 1);
@@ -148,11 +163,15 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
             mb_wait(&dbar, 0);
             int s = 0;
             unsigned ph = 0;
-            for (int m = 0; m < mine; ++m) {
+            for (int u = 0; u < NPASS * mine; ++u) {
+                int m, second;
+                seq(u, mine, m, second);
                 const int ab = m & 1;
-                mb_wait(&acce[ab], ((m >> 1) & 1) ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t td = tmem + ab * NN;
+                if (!second) {
+                    mb_wait(&acce[ab], ((m >> 1) & 1) ^ 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;");
+                }
+                const uint32_t td = second ? tmem + 32 : tmem + ab * NN;
                 for (int c = 0; c < nchunk; ++c) {
                     mb_wait(&full[s], ph);
                     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -177,7 +196,7 @@ __global__ void __launch_bounds__(192, 1) k_phase1(const __half* __restrict__ Yc
                         ph ^= 1;
                     }
                 }
-                commit(&accf[ab]);
+                if (!second) commit(&accf[ab]);
             }
         }
     } else {  // warps 2..5: TMEM lanes 32 * (warp % 4)
