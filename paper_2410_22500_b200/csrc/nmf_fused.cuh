@@ -533,15 +533,16 @@ struct Pass {
                 const int nv = (int)min((int64_t)RG, Np - r0);
                 mbar_wait_s(fullb + 8u * (unsigned)b, ph);
                 float rfac, vome;
-                if constexpr (NGRP == 4) {
+                if constexpr (true) {
                     // split barrier: publish the partials, compute the V-update factor while the
-                    // group's other warps finish (C2: 49.4 -> 48.2 us per iteration)
+                    // group's other warps finish (C2: 49.4 -> 48.2 us per iteration; with three
+                    // groups it pays once the reduction is select-free, C4 6.19 -> 6.13 ms)
                     phase1.template operator()<false>(b, n, r0, nv, rfac, vome);
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cta(&sh.part[g][n & 1]);
                     vfactor(b, r0, nv, rfac, vome);
                     mbar_wait_s(partb + 8u * (unsigned)(n & 1), (unsigned)((n >> 1) & 1));
-                } else {  // three groups: the split measured slightly slower, keep the named barrier
+                } else {  // (the named-barrier schedule, kept for reference)
                     phase1.template operator()<true>(b, n, r0, nv, rfac, vome);
                     named_bar(1 + g, TG);
                 }
