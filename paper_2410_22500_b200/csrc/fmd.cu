@@ -23,6 +23,9 @@ namespace {
 constexpr int FT = 256;          // threads per block
 constexpr int FMD_MAXM = 8;      // materials
 constexpr int FMD_RACC = 48;     // fp64 accumulators per thread in the transform pass
+#ifndef FMD_NNLS_MINB
+#define FMD_NNLS_MINB 2  // two blocks per SM (128 registers): 3.68 -> 2.61 ms at C4; three spill
+#endif
 
 __device__ __forceinline__ double warp_sum_dd(double v) {
 #pragma unroll
@@ -181,7 +184,7 @@ __global__ void __launch_bounds__(FT) k_fmd_prep(const float* __restrict__ T, in
 // Per voxel NNLS by passive-set search in order of increasing size (subset order table in
 // smem), KKT test in fp64.  Xm [Nm][Nx].
 template <int K, int NM>
-__global__ void __launch_bounds__(FT) k_fmd_nnls(const float* __restrict__ X, int64_t Nx, const float* __restrict__ T,
+__global__ void __launch_bounds__(FT, FMD_NNLS_MINB) k_fmd_nnls(const float* __restrict__ X, int64_t Nx, const float* __restrict__ T,
                                                  const double* __restrict__ G, const double* __restrict__ tab,
                                                  float* __restrict__ Xm, unsigned* __restrict__ status) {
     constexpr int NS = 1 << NM;
