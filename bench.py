@@ -305,10 +305,18 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     ramp_bytes = 4.0 * K * Np + 4.0 * kc * Np                  # read V, write Q
     bp_smem_bytes = 2.0 * 4 * K * Nx * cfg.Nv                  # two detector samples per voxel, view, channel
     smem_peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e9    # GB/s: 128 B/clk/SM (B300_MICROARCH.md)
+    fp32_peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12  # TFLOP/s: 128 FMA/clk/SM
+    P = 1 << max(1, (2 * cfg.Nc - 1).bit_length())
+    ramp_flops = (cfg.Nv * cfg.Nr) * ((K + 1) // 2) * (2 * 5.0 * P * math.log2(P) + 2.0 * P)
     stages.update({
         "ramp_s": t_ramp, "backproject_s": t_bp,
         "ramp_roofline": {"bound": "hbm", "achieved": ramp_bytes / t_ramp / 1e9, "peak": peaks["hbm_gbs"],
-                          "unit": "GB/s", "frac": ramp_bytes / t_ramp / 1e9 / peaks["hbm_gbs"]},
+                          "unit": "GB/s", "frac": ramp_bytes / t_ramp / 1e9 / peaks["hbm_gbs"],
+                          # the FFT arithmetic that actually bounds it: 5 P log2 P flop per complex
+                          # transform, forward + inverse, one per channel pair and detector row,
+                          # plus the real filter product; against the FP32 FMA peak
+                          "alu_tflops": ramp_flops / t_ramp / 1e12, "alu_peak_tflops": fp32_peak,
+                          "alu_frac": ramp_flops / t_ramp / 1e12 / fp32_peak},
         "backproject_roofline": {"bound": "smem", "achieved": bp_smem_bytes / t_bp / 1e9, "peak": smem_peak,
                                  "unit": "GB/s", "frac": bp_smem_bytes / t_bp / 1e9 / smem_peak,
                                  "hbm_frac": (4.0 * kc * Np + 4.0 * K * Nx) / t_bp / 1e9 / peaks["hbm_gbs"],
