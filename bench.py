@@ -29,8 +29,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
-METRIC = "hyperspectral voxel*lambda reconstructed/sec (1xB200) + % roofline per stage"
-UNIT = "voxel*lambda/s"
+METRIC = "hyperspectral voxel\u00b7\u03bb reconstructed/sec (1\u00d7B200) + % roofline per stage"  # BASELINE.json
+UNIT = "voxel\u00b7\u03bb/s"
 
 
 def parse():
