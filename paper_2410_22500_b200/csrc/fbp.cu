@@ -23,10 +23,11 @@ namespace hsnct {
 namespace {
 
 constexpr int RT = 256;      // ramp-filter threads
-constexpr int BTX = 16, BTY = 32;  // backprojection voxel tile (columns x rows)
+constexpr int BTX = 16;            // backprojection voxel tile: 16 columns x 16 VPT rows
 // detector window per view per tile: the tile's voxels span <= 15|cos| + 31|sin| <= 34.4 bins,
 // plus the interpolation neighbour and a one-bin margin on each side of floor()
-constexpr int BWMAX = 40;
+// (16 x 16 tiles: <= 15(|cos| + |sin|) + 3 <= 24.3 -> 28)
+__host__ __device__ constexpr int bp_wmax(int VPT) { return VPT == 2 ? 40 : 28; }
 constexpr int BVMAX = 64;          // views per staged chunk (upper bound)
 // floats per staged detector sample: KC, plus 4 when KC is a multiple of 8 (an odd number
 // of 16-byte chunks per sample spreads a quarter-warp's LDS.128 over all bank groups; the
@@ -330,12 +331,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // each, stored exactly as in Q so a window is one contiguous run of floats) is staged by
 // cp.async into one of two buffers while the other chunk is being used.  Per voxel and view:
 // u = x cos + y sin + (N_c - 1)/2, l = floor(u), w = u - l, acc += (1 - w) q[l] + w q[l + 1].
-template <int KC>
-__global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
+template <int KC, int VPT>
+__global__ void __launch_bounds__(BTX * 16, KC <= 8 ? 4 : 2) k_backproject(
     const float* __restrict__ Q, int NchAll, int Nv, int Nc, int s0, int ns, const float* __restrict__ cos_t,
     const float* __restrict__ sin_t, int mode, float* __restrict__ out, int64_t ld_out, int64_t col0,
     int64_t Nx, int vch) {
-    constexpr int NT = BTX * BTY / 2;
+    constexpr int NT = BTX * 16;
+    constexpr int BTY = 16 * VPT;      // tile rows; VPT voxels per thread (rows ty, ty + 16)
+    constexpr int BWMAX = bp_wmax(VPT);
     constexpr int VEC = KC % 4 == 0 ? 4 : (KC % 2 == 0 ? 2 : 1);  // floats per copy (global alignment)
     constexpr int SP = bp_pitch(KC);                               // floats per staged sample
     constexpr int LV = SP % 4 == 0 ? 4 : (SP % 2 == 0 ? 2 : 1);    // floats per shared-memory load
@@ -439,15 +442,15 @@ __global__ void __launch_bounds__(BTX * BTY / 2, KC <= 8 ? 4 : 2) k_backproject(
             const float u1 = fmaf(x, t.x, fmaf(y1, t.y, half));
             const float f0 = floorf(u0), f1 = floorf(u1);
             interp(acc0, win + vv * WIN + ((int)f0 - cl) * SP, u0 - f0);
-            interp(acc1, win + vv * WIN + ((int)f1 - cl) * SP, u1 - f1);
+            if constexpr (VPT == 2) interp(acc1, win + vv * WIN + ((int)f1 - cl) * SP, u1 - f1);
         }
         __syncthreads();  // buffer b is refilled by the next iteration's prefetch
     }
     if (j >= Nc) return;
     const float scale = 3.14159265358979323846f / (float)Nv;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int i = i0 + q * (BTY / 2);
+    for (int q = 0; q < VPT; ++q) {
+        const int i = i0 + q * 16;
         if (i >= Nc) break;
         const float2* acc = q ? acc1 : acc0;
         if (mode == 0) {
@@ -510,24 +513,34 @@ cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* i
     return cudaGetLastError();
 }
 
-template <int KC>
-static cudaError_t bp_k(const Geometry& g, const DeviceTables& t, const float* Q, int Nch, int s0,
-                        int ns, int mode, float* out, int64_t ld_out, int64_t col0, cudaStream_t s) {
+template <int KC, int VPT>
+static cudaError_t bp_kv(const Geometry& g, const DeviceTables& t, const float* Q, int Nch, int s0, int ns, int mode,
+                         float* out, int64_t ld_out, int64_t col0, cudaStream_t s) {
     // views per chunk: two buffers of about 20 KB (KC <= 8: four blocks per SM) or 40 KB
     // (KC = 16: two blocks per SM, 128 registers) each
-    const int per_view = BWMAX * bp_pitch(KC) * (int)sizeof(float);
+    const int per_view = bp_wmax(VPT) * bp_pitch(KC) * (int)sizeof(float);
     const int vch = std::max(1, std::min(std::min(g.Nv, BVMAX), ((KC <= 8 ? 20 : 40) * 1024) / per_view));
     const size_t smem = (size_t)2 * vch * per_view;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_backproject<KC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        cudaFuncSetAttribute(k_backproject<KC, VPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
     const int nchunk = (Nch + KC - 1) / KC;
-    dim3 grid((g.Nc + BTX - 1) / BTX, (g.Nc + BTY - 1) / BTY, ns * nchunk);
-    k_backproject<KC><<<grid, BTX * BTY / 2, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode, out,
-                                                       ld_out, col0, (int64_t)g.Nr * g.Nc * g.Nc, vch);
+    dim3 grid((g.Nc + BTX - 1) / BTX, (g.Nc + 16 * VPT - 1) / (16 * VPT), ns * nchunk);
+    k_backproject<KC, VPT><<<grid, BTX * 16, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode, out,
+                                                        ld_out, col0, (int64_t)g.Nr * g.Nc * g.Nc, vch);
     return cudaGetLastError();
+}
+
+// Two voxels per thread (16 x 32 tiles) unless that leaves fewer than two blocks per SM
+// (C1, C2: one slice), then 16 x 16 tiles with one voxel per thread.
+template <int KC>
+static cudaError_t bp_k(const Geometry& g, const DeviceTables& t, const float* Q, int Nch, int s0, int ns, int mode,
+                        float* out, int64_t ld_out, int64_t col0, cudaStream_t s) {
+    const int64_t blocks2 = (int64_t)((g.Nc + BTX - 1) / BTX) * ((g.Nc + 31) / 32) * ns * ((Nch + KC - 1) / KC);
+    if (blocks2 < 2 * (int64_t)g.num_sms) return bp_kv<KC, 1>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
+    return bp_kv<KC, 2>(g, t, Q, Nch, s0, ns, mode, out, ld_out, col0, s);
 }
 
 cudaError_t backproject(const Geometry& g, const DeviceTables& t, const float* Q, int Kc, int Nch,
