@@ -225,6 +225,101 @@ __global__ void __launch_bounds__(FT, FMD_NNLS_MINB) k_fmd_nnls(const float* __r
         const double tol = 1e-12 * bmax;
         double x[NM], best[NM], fbest = 1e300;
         bool found = false;
+        // x_P = inv(G_PP) b_P (zero off P); true when every x_P > 0
+        auto solve = [&](int P, double* z) {
+            const int mP = __popc(P);
+            const double* Ip = inv + offs[P];
+            bool pos = true;
+            int a = 0;
+#pragma unroll
+            for (int i = 0; i < NM; ++i) {
+                z[i] = 0.0;
+                if (P & (1 << i)) {
+                    double s = 0.0;
+                    int c2 = 0;
+#pragma unroll
+                    for (int j = 0; j < NM; ++j)
+                        if (P & (1 << j)) s = fma(Ip[a * mP + c2++], b[j], s);
+                    z[i] = s;
+                    pos = pos && (s > 0.0);
+                    ++a;
+                }
+            }
+            return pos;
+        };
+        // Lawson-Hanson active set first: a few passive-set solves per voxel instead of up to
+        // 2^NM. It accepts only a solve with x_P > 0 whose off-set gradient is <= tol -- the
+        // enumeration's KKT test, so both return the unique solution; any stall (an added index
+        // that cannot stay, the iteration cap) hands the voxel to the enumeration below.
+        {
+            int P = 0, banned = 0;
+            bool sol = true, stall = false;
+            double xl[NM];
+#pragma unroll
+            for (int i = 0; i < NM; ++i) xl[i] = 0.0;
+            for (int it = 0; it < 2 * NM && !found && !stall; ++it) {
+                int jb = -1;
+                double wb = tol;
+#pragma unroll
+                for (int j = 0; j < NM; ++j) {
+                    double g = b[j];
+#pragma unroll
+                    for (int i = 0; i < NM; ++i) g = fma(-Gs[j * NM + i], xl[i], g);
+                    if (!((P | banned) & (1 << j)) && g > wb) {
+                        wb = g;
+                        jb = j;
+                    }
+                }
+                if (jb < 0) {
+                    if (sol && !banned) {
+#pragma unroll
+                        for (int i = 0; i < NM; ++i) x[i] = xl[i];
+                        found = true;
+                    } else {
+                        stall = true;
+                    }
+                    break;
+                }
+                P |= 1 << jb;
+                sol = false;
+                for (int inner = 0; inner < NM && P && !stall; ++inner) {
+                    double z[NM];
+                    if (solve(P, z)) {
+#pragma unroll
+                        for (int i = 0; i < NM; ++i) xl[i] = z[i];
+                        sol = true;
+                        break;
+                    }
+                    if (z[jb] <= 0.0 && inner == 0) {  // the new index cannot enter: give up
+                        stall = true;
+                        banned |= 1 << jb;
+                        break;
+                    }
+                    double alpha = 1.0;
+                    int imin = -1;
+#pragma unroll
+                    for (int i = 0; i < NM; ++i)
+                        if ((P & (1 << i)) && z[i] <= 0.0) {
+                            const double ai = xl[i] / (xl[i] - z[i]);
+                            if (ai < alpha || imin < 0) {
+                                alpha = ai;
+                                imin = i;
+                            }
+                        }
+#pragma unroll
+                    for (int i = 0; i < NM; ++i) xl[i] = fma(alpha, z[i] - xl[i], xl[i]);
+                    xl[imin] = 0.0;  // the blocking index leaves the set
+#pragma unroll
+                    for (int i = 0; i < NM; ++i)
+                        if ((P & (1 << i)) && (i == imin || xl[i] <= 0.0)) {
+                            P &= ~(1 << i);
+                            xl[i] = 0.0;
+                        }
+                }
+                if (!sol && !P) sol = true;  // back to the empty set: x = 0 is its solve
+                if (!sol) stall = true;
+            }
+        }
         for (int q = 0; q < NS && !found; ++q) {
             const int P = order[q];
             const int mP = __popc(P);

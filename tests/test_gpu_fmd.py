@@ -101,3 +101,24 @@ def test_fmd_errors():
     with pytest.raises(HsnctError) as e:
         h.sync()
     assert e.value.status == 2
+
+
+def test_fmd_nnls_random_supports():
+    """Eq. 8 on random mixed-sign x^s with N_m = K = 6: solutions of every support size (the
+    Lawson-Hanson front end and its enumeration fallback), vs the oracle's NNLS."""
+    cfg = sd.custom(idx=31, Nc=48, Nv=8, Nr=2, Nk=12, K=6, M=6)
+    g = np.random.default_rng(11)
+    K = Nm = 6
+    T = (np.eye(Nm, K) + 0.3 * g.random((Nm, K))).astype(np.float32)
+    X = g.standard_normal((K, cfg.Nx)).astype(np.float32)
+    h = hs(cfg)
+    Xd = torch.as_tensor(X).reshape(K, cfg.Nr, cfg.Nc, cfg.Nc).to(DEV).contiguous()
+    Xm = h.fmd_materials(Xd, torch.as_tensor(T).to(DEV))
+    h.sync()
+    Xmo = oracle.fmd_materials(X.reshape(K, cfg.Nr, cfg.Nc, cfg.Nc), T)
+    a = Xm.reshape(Nm, -1).cpu().double().numpy()
+    b = np.asarray(Xmo, np.float64).reshape(Nm, -1)
+    assert rel(a, b) <= 1e-5, rel(a, b)
+    assert np.abs(a - b).max() <= 1e-4 * max(1.0, np.abs(b).max())
+    supp = (b > 0).sum(axis=0)
+    assert set(np.unique(supp)) >= {0, 1, 2, 3, 4}  # the data really exercise many support sizes
