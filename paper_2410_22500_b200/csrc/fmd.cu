@@ -37,7 +37,7 @@ __device__ __forceinline__ double warp_sum_dd(double v) {
 // thread t takes voxels t, t + FT, ... of the range (fixed order), then a fixed-order
 // block reduction.  part[b][i - i0][k] (fp64), cnt[b][i - i0] (int64).
 template <int K, int RMAX>
-__global__ void __launch_bounds__(FT) k_fmd_tpart(const float* __restrict__ X, int64_t Nx,
+__global__ void __launch_bounds__(FT, 2) k_fmd_tpart(const float* __restrict__ X, int64_t Nx,
                                                   const int32_t* __restrict__ labels, int Nm, int i0, int nr,
                                                   int64_t per_blk, double* __restrict__ part,
                                                   long long* __restrict__ cnt, unsigned* __restrict__ status) {
