@@ -23,6 +23,8 @@ namespace hsnct {
 namespace {
 
 constexpr int RT = 256;      // ramp-filter threads
+// k_ramp_reg: three blocks per SM (80 registers) for P <= 512 (C3 0.062 -> 0.055 ms), two
+// for P = 1024, whose 32-point transforms need the registers (three: C4 0.122 -> 0.131 ms)
 constexpr int BTX = 16;            // backprojection voxel tile: 16 columns x 16 VPT rows
 // detector window per view per tile: the tile's voxels span <= 15|cos| + 31|sin| <= 34.4 bins,
 // plus the interpolation neighbour and a one-bin margin on each side of floor()
@@ -235,7 +237,7 @@ __device__ __forceinline__ float2 twp(const float2* __restrict__ tw, int m, int 
 }
 
 template <int B>
-__global__ void __launch_bounds__(256, 2) k_ramp_reg(const float* __restrict__ in, int64_t ld_in, int NchAll,
+__global__ void __launch_bounds__(256, B <= 16 ? 3 : 2) k_ramp_reg(const float* __restrict__ in, int64_t ld_in, int NchAll,
                                                     int Nv, int Nr, int Nc, int s0, int ns,
                                                     const float* __restrict__ Hhat,
                                                     const float2* __restrict__ tw, float* __restrict__ Q,
