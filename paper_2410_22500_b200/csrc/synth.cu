@@ -81,29 +81,38 @@ __global__ void __launch_bounds__(ST) k_synth_v(const float* __restrict__ X, con
                                                 int Nk, int64_t n0, int64_t nn, int b0, int nb,
                                                 float* __restrict__ Xh, int64_t ld) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int q = blockIdx.y * 32 + lane;  // bin quad of this lane
     const int nq = (nb + 3) >> 2;
-    const bool act = q < nq;
-    float4 d[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        float v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int b = 4 * q + e;
-            v[e] = (act && b < nb) ? __ldg(D + (int64_t)k * Nk + b0 + b) : 0.f;
-        }
-        d[k] = make_float4(v[0], v[1], v[2], v[3]);
-    }
-    const bool full = 4 * q + 3 < nb;
+    const int nqg = (nq + 31) >> 5;                    // bin groups of 32 quads
     const int64_t nchunk = (nn + 31) >> 5;
+    const int64_t nunits = nchunk * nqg;               // unit = (voxel chunk, bin group), group fastest
     const int64_t wstride = (int64_t)gridDim.x * (ST / 32);
     // this warp's X chunk, k-major, so that one broadcast LDS.128 serves four voxels
     __shared__ __align__(16) float xs[ST / 32][K][32];
-    for (int64_t ch = (int64_t)blockIdx.x * (ST / 32) + warp; ch < nchunk; ch += wstride) {
+    int grp = -1, q = 0;
+    bool act = false, full = false;
+    float4 d[K];
+    for (int64_t u = (int64_t)blockIdx.x * (ST / 32) + warp; u < nunits; u += wstride) {
+        const int g = (int)(u % nqg);
+        const int64_t ch = u / nqg;
+        if (g != grp) {  // this lane's bin quad and its D values
+            grp = g;
+            q = g * 32 + lane;
+            act = q < nq;
+            full = 4 * q + 3 < nb;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                float v[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int b = 4 * q + e;
+                    v[e] = (act && b < nb) ? __ldg(D + (int64_t)k * Nk + b0 + b) : 0.f;
+                }
+                d[k] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+        }
         const int64_t nb0 = ch << 5;
         const int cnt = (int)min((int64_t)32, nn - nb0);
-        __syncwarp();  // the previous chunk's reads of xs are done
+        __syncwarp();  // the previous unit's reads of xs are done
 #pragma unroll
         for (int k = 0; k < K; ++k) xs[warp][k][lane] = lane < cnt ? __ldg(X + (int64_t)k * Nx + n0 + nb0 + lane) : 0.f;
         __syncwarp();
@@ -153,12 +162,10 @@ cudaError_t synth_k(const Geometry& g, const float* X, const float* D, int s0, i
     const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(want, (per_col + ST - 1) / ST));
     dim3 grid(nblk, ncol);
     const bool vec = ((reinterpret_cast<uintptr_t>(Xh) & 15) == 0) && (ld % 4 == 0);
-    if (vec) {
-        const int nqg = (nb + 127) / 128;
-        const int64_t wblocks = ((nn + 31) / 32 + (ST / 32) - 1) / (ST / 32);
-        const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 8) / nqg);
-        dim3 gv((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, wblocks)), nqg);
-        k_synth_v<K><<<gv, ST, 0, s>>>(X, D, Nx, g.Nk, n0, nn, b0, nb, Xh, ld);
+    if (vec) {  // one flat list of (voxel chunk, bin group) units over num_sms x 8 blocks
+        const int64_t nunits = ((nn + 31) / 32) * ((nb + 127) / 128);
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (nunits + 7) / 8));
+        k_synth_v<K><<<(unsigned)blocks, ST, 0, s>>>(X, D, Nx, g.Nk, n0, nn, b0, nb, Xh, ld);
         return cudaGetLastError();
     }
     if (vec)
