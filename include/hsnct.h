@@ -24,7 +24,8 @@
  *                     bin index fastest.  ld_y >= N_k, ld_y % 4 == 0,
  *                     16-byte aligned; all N_p*ld_y floats must be readable (the
  *                     padding columns are read and ignored).
- *   V   [N_p][K]      subspace views V^s, row p as for Y.
+ *   V   [N_p][K]      subspace views V^s, row p as for Y; 16-byte
+ *                     aligned in hsnct_subspace_decompose (rows are bulk-copied).
  *   D   [K][N_k]      subspace basis, stored as (D^s)^T.
  *   X   [K][N_r][N_c][N_c]  subspace reconstructions x^s,
  *                     channel-planar; voxel (r, i, j) at x = j-(N_c-1)/2,
@@ -90,8 +91,9 @@ typedef enum {
 typedef struct {
     int32_t n_views; /* N_v >= 2                 */
     int32_t n_rows;  /* N_r >= 1                 */
-    int32_t n_cols;  /* 2 <= N_c <= 2048         */
-    int32_t n_bins;  /* N_k >= 1                 */
+    int32_t n_cols;  /* 2 <= N_c <= 1024 (FFT length P = next_pow2(2 N_c) <= 2048) */
+    int32_t n_bins;  /* N_k >= 1, and K * round_up(N_k, 4) <= 51200 (the row pass
+                        keeps D [K][N_k] in shared memory)                       */
     int32_t n_sub;   /* 1 <= K <= min(16, N_k)   */
     const double* angles; /* HOST array of N_v view angles in radians, copied at create;
                              NULL => theta_v = v*pi/N_v (R13)            */
@@ -155,6 +157,24 @@ hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const 
                             const float* D0_host, int n_iter, float* Xh_host, float* V_host,
                             float* D_host, void* ws, size_t ws_bytes, void* stream);
 
+/* Algorithm 1 end to end on HOST buffers for volumes whose x^h does not fit in host or
+ * device memory (C4: 215 GB, C5: 430 GB): like hsnct_fhr_host, but x^h leaves the device in
+ * windows of window_slices slices (all N_k bins) through a caller-owned page-locked HOST
+ * ring of two windows, ring_host [2][window_slices*N_c*N_c][N_k].  Window w is synthesized
+ * on `stream` into one of two device window buffers while window w-1 is copied D2H on a
+ * second stream of the handle; when window w's copy has completed, on_window(user, slice0,
+ * n_slices, xh) is called on the calling thread with xh pointing into the ring (valid until
+ * the call returns; the slot is then reused for window w+2).  on_window may be NULL.
+ * Workspace: hsnct_fhr_stream_bytes(h, window_slices).  V_host / D_host nullable as in
+ * hsnct_fhr_host.  Blocks until the last window has been delivered; returns the deferred
+ * data/numeric status like hsnct_sync. */
+typedef void (*hsnct_window_fn)(void* user, int slice0, int n_slices, const float* xh);
+size_t hsnct_fhr_stream_bytes(hsnct_t h, int window_slices);
+hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
+                              const float* D0_host, int n_iter, int window_slices, float* ring_host,
+                              hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
+                              void* ws, size_t ws_bytes, void* stream);
+
 /* ---- Fast material decomposition, semi-supervised back half (NEXT-2):
  * Algorithm 2 after the subspace reconstruction, on X
  * [K][N_x] (hsnct_fbp's output).  1 <= n_mat <= min(K, 8).  Workspace:
@@ -196,6 +216,13 @@ uint64_t hsnct_kernel_launches(hsnct_t h);
  * receives the number available (0 when tracing is off), *n_cta the CTA count
  * (both nullable).  Synchronous. */
 hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta);
+
+/* Diagnostics: the subspace-extraction plan chosen at create (which row-pass kernel, its
+ * template parameters and grid), as a NUL-terminated string copied to the HOST buffer
+ * buf (at most n bytes, truncated).  Shapes that differ only in N_r beyond a few row
+ * tiles select the same plan; the GPU tests use this to show that the slice-reduced
+ * full-iteration parity configs run the bench configs' kernels. */
+hsnct_status hsnct_debug_plan(hsnct_t h, char* buf, size_t n);
 
 /* Diagnostics: stage timing of hsnct_fbp (bench.py's per-stage rooflines).
  * hsnct_debug_fbp_timing(h, 1) makes every later hsnct_fbp call record CUDA events

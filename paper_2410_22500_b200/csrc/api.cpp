@@ -31,6 +31,9 @@ struct hsnct_s {
     int trace_iters = 0;
     cudaEvent_t fbp_ev[3] = {nullptr, nullptr, nullptr};  // stage timing of hsnct_fbp (diagnostics)
     bool fbp_timed = false;                               // events of the last call are recorded
+    // hsnct_fhr_stream: D2H copy stream and per-window-buffer events (created on first use)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_syn[2] = {nullptr, nullptr}, ev_cpy[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -119,6 +122,15 @@ FhrHostLayout fhr_layout(const Geometry& g, const NmfPlan& p) {
     return L;
 }
 
+// hsnct_fhr_stream: as fhr_layout, with two device windows of window_slices slices
+FhrHostLayout stream_layout(const Geometry& g, const NmfPlan& p, int window_slices) {
+    FhrHostLayout L = fhr_layout(g, p);
+    L.total -= L.xh;
+    L.xh = a256((size_t)window_slices * g.Nc * g.Nc * g.Nk * sizeof(float));
+    L.total += 2 * L.xh;
+    return L;
+}
+
 hsnct_status check_ws(void* ws, size_t have, size_t need, const char* op) {
     if (need == 0) return HSNCT_OK;
     if (!ws) return fail(HSNCT_E_ARG, "%s: workspace is NULL (need %zu bytes)", op, need);
@@ -153,18 +165,6 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
     w.trace_iters = h->trace_iters;
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
-    if (h->nmf.mma) {
-        const int nbx = (h->g.Nk + 31) / 32;
-        cudaError_t e = nmf_mma_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1, h->t.status, s);
-        if (e == cudaSuccess) {
-            h->launches += 1;
-            return HSNCT_OK;
-        }
-        // cooperative launch refused: redo the input preparation for the FFMA path below
-        (void)cudaGetLastError();
-        CK(nmf_yplus_launch(h->g, h->nmf, w, Y, ld, h->t.status, s), "decompose init (fallback)");
-        h->launches += 1;
-    }
     if (h->nmf.persist) {
         const int nbx = (h->g.Nk + 31) / 32;
         cudaError_t e = nmf_persist_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1,
@@ -208,11 +208,13 @@ hsnct_status read_status(hsnct_t h, cudaStream_t s) {
         CK(cudaMemsetAsync(h->t.status, 0, sizeof(unsigned), s), "sync");
         CK(cudaStreamSynchronize(s), "sync");
     }
-    if (st & (ST_Y_NONFINITE | ST_Y_ALLZERO | ST_INIT_BAD))
-        return fail(HSNCT_E_DATA, "data error (status 0x%x):%s%s%s", st,
+    if (st & (ST_Y_NONFINITE | ST_Y_ALLZERO | ST_INIT_BAD | ST_LABEL_BAD | ST_REGION_EMPTY))
+        return fail(HSNCT_E_DATA, "data error (status 0x%x):%s%s%s%s%s", st,
                     (st & ST_Y_NONFINITE) ? " non-finite Y;" : "",
                     (st & ST_Y_ALLZERO) ? " Y+ is identically zero;" : "",
-                    (st & ST_INIT_BAD) ? " V0/D0 non-finite or negative;" : "");
+                    (st & ST_INIT_BAD) ? " V0/D0 non-finite or negative;" : "",
+                    (st & ST_LABEL_BAD) ? " FMD label outside [-1, n_mat);" : "",
+                    (st & ST_REGION_EMPTY) ? " an FMD user region is empty;" : "");
     if (st & ST_NUMERIC) return fail(HSNCT_E_NUMERIC, "numerical error: NaN/Inf produced in V or D");
     return HSNCT_OK;
 }
@@ -362,6 +364,11 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->trace);
     for (cudaEvent_t e : h->fbp_ev)
         if (e) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_syn[i]) cudaEventDestroy(h->ev_syn[i]);
+        if (h->ev_cpy[i]) cudaEventDestroy(h->ev_cpy[i]);
+    }
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
     if (h->status_host) cudaFreeHost(h->status_host);
     delete h;
 }
@@ -387,7 +394,9 @@ hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, f
     hsnct_status st = check_y(g, Y, ld_y, "decompose");
     if (st) return st;
     if (!V || !D) return fail(HSNCT_E_ARG, "decompose: V or D is NULL");
-    if (!aligned(V, 4) || !aligned(D, 4)) return fail(HSNCT_E_ARG, "decompose: V, D must be 4-byte aligned");
+    // V rows are bulk-copied (cp.async.bulk) by the row-pass kernels: 16-byte aligned base
+    if (!aligned(V, 16) || !aligned(D, 4))
+        return fail(HSNCT_E_ARG, "decompose: V must be 16-byte aligned and D 4-byte aligned");
     if (n_iter < 0) return fail(HSNCT_E_ARG, "decompose: n_iter=%d < 0", n_iter);
     if (obj_trace && !aligned(obj_trace, 8)) return fail(HSNCT_E_ARG, "decompose: obj_trace misaligned");
     const size_t need = a256(nmf_ws_bytes(g, h->nmf));
@@ -536,6 +545,94 @@ hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const 
     return read_status(h, s);
 }
 
+size_t hsnct_fhr_stream_bytes(hsnct_t h, int window_slices) {
+    if (!h || window_slices < 1) return 0;
+    return stream_layout(h->g, h->nmf, std::min(window_slices, h->g.Nr)).total;
+}
+
+hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
+                              const float* D0_host, int n_iter, int window_slices, float* ring_host,
+                              hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
+                              void* ws, size_t ws_bytes, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "fhr_stream: handle is NULL");
+    const Geometry& g = h->g;
+    if (!Y_host || !V0_host || !D0_host || !ring_host)
+        return fail(HSNCT_E_ARG, "fhr_stream: Y, V0, D0 and the ring are required");
+    if (ld_y < g.Nk) return fail(HSNCT_E_ARG, "fhr_stream: ld_y=%lld < N_k=%d", (long long)ld_y, g.Nk);
+    if (n_iter < 0) return fail(HSNCT_E_ARG, "fhr_stream: n_iter=%d < 0", n_iter);
+    if (window_slices < 1) return fail(HSNCT_E_ARG, "fhr_stream: window_slices=%d < 1", window_slices);
+    const int wsl = std::min(window_slices, g.Nr);
+    const FhrHostLayout L = stream_layout(g, h->nmf, wsl);
+    hsnct_status st = check_ws(ws, ws_bytes, L.total, "fhr_stream");
+    if (st) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!h->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "fhr_stream stream");
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventCreateWithFlags(&h->ev_syn[i], cudaEventDisableTiming), "fhr_stream events");
+            CK(cudaEventCreateWithFlags(&h->ev_cpy[i], cudaEventDisableTiming), "fhr_stream events");
+        }
+    }
+    char* c = static_cast<char*>(ws);
+    float* Yd = (float*)c;
+    c += L.y;
+    float* Vd = (float*)c;
+    c += L.v;
+    float* Dd = (float*)c;
+    c += L.d;
+    float* Xd = (float*)c;
+    c += L.x;
+    float* Xw[2] = {(float*)c, (float*)(c + L.xh)};
+    c += 2 * L.xh;
+    void* wn = c;
+    c += L.nmf;
+    void* wf = c;
+    const int64_t Np = Np_of(g);
+    CK(cudaMemcpy2DAsync(Yd, (size_t)L.Nkp * sizeof(float), Y_host, (size_t)ld_y * sizeof(float),
+                         (size_t)g.Nk * sizeof(float), (size_t)Np, cudaMemcpyHostToDevice, s),
+       "fhr_stream H2D Y");
+    CK(cudaMemcpyAsync(Vd, V0_host, (size_t)Np * g.K * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_stream H2D V0");
+    CK(cudaMemcpyAsync(Dd, D0_host, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_stream H2D D0");
+    if ((st = run_decompose(h, Yd, L.Nkp, Vd, Dd, n_iter, nullptr, wn, s))) return st;
+    if ((st = run_fbp(h, Vd, Xd, wf, s))) return st;
+    if (V_host)
+        CK(cudaMemcpyAsync(V_host, Vd, (size_t)Np * g.K * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_stream D2H V");
+    if (D_host)
+        CK(cudaMemcpyAsync(D_host, Dd, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_stream D2H D");
+    const size_t slice_elems = (size_t)g.Nc * g.Nc * g.Nk;
+    const int nwin = (g.Nr + wsl - 1) / wsl;
+    auto deliver = [&](int w) -> hsnct_status {
+        CK(cudaEventSynchronize(h->ev_cpy[w & 1]), "fhr_stream D2H");
+        const int s0 = w * wsl, ns = std::min(wsl, g.Nr - s0);
+        if (on_window) on_window(user, s0, ns, ring_host + (size_t)(w & 1) * wsl * slice_elems);
+        return HSNCT_OK;
+    };
+    for (int w = 0; w < nwin; ++w) {
+        const int b = w & 1;
+        const int s0 = w * wsl, ns = std::min(wsl, g.Nr - s0);
+        if (w >= 2) {  // window w-2 used this device buffer and host slot: wait for its copy
+            if ((st = deliver(w - 2))) return st;
+            CK(cudaStreamWaitEvent(s, h->ev_cpy[b], 0), "fhr_stream order");
+        }
+        CK(synthesize(g, Xd, Dd, s0, ns, 0, g.Nk, Xw[b], g.Nk, s), "fhr_stream synthesize");
+        h->launches += 1;
+        CK(cudaEventRecord(h->ev_syn[b], s), "fhr_stream order");
+        CK(cudaStreamWaitEvent(h->copy_stream, h->ev_syn[b], 0), "fhr_stream order");
+        CK(cudaMemcpyAsync(ring_host + (size_t)b * wsl * slice_elems, Xw[b], (size_t)ns * slice_elems * sizeof(float),
+                           cudaMemcpyDeviceToHost, h->copy_stream),
+           "fhr_stream D2H Xh");
+        CK(cudaEventRecord(h->ev_cpy[b], h->copy_stream), "fhr_stream order");
+    }
+    for (int w = std::max(0, nwin - 2); w < nwin; ++w)
+        if ((st = deliver(w))) return st;
+    // the caller's stream must not run ahead of the last copies (the device windows are its workspace)
+    CK(cudaStreamWaitEvent(s, h->ev_cpy[(nwin - 1) & 1], 0), "fhr_stream order");
+    if (nwin >= 2) CK(cudaStreamWaitEvent(s, h->ev_cpy[(nwin - 2) & 1], 0), "fhr_stream order");
+    return read_status(h, s);
+}
+
 static hsnct_status check_nmat(const Geometry& g, int n_mat, const char* op) {
     if (n_mat < 1 || n_mat > std::min(g.K, 8))
         return fail(HSNCT_E_ARG, "%s: n_mat=%d outside [1, min(K=%d, 8)]", op, n_mat, g.K);
@@ -622,6 +719,17 @@ hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_ou
     if (!host) return fail(HSNCT_E_ARG, "debug_trace: host buffer is NULL");
     DeviceGuard guard(h->device);
     CK(cudaMemcpy(host, h->trace, m * sizeof(uint64_t), cudaMemcpyDeviceToHost), "debug_trace");
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_debug_plan(hsnct_t h, char* buf, size_t n) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_plan: handle is NULL");
+    if (!buf || n == 0) return fail(HSNCT_E_ARG, "debug_plan: buffer is NULL or empty");
+    const std::string d = nmf_plan_desc(h->g, h->nmf);
+    const size_t m = std::min(n - 1, d.size());
+    memcpy(buf, d.data(), m);
+    buf[m] = 0;
     return HSNCT_OK;
 }
 

@@ -477,11 +477,9 @@ static cudaError_t ramp_reg(const Geometry& g, const DeviceTables& t, const floa
                             int s0, int ns, float* Q, int Kc, cudaStream_t s) {
     const int npair = (std::min(Nch, Kc) + 1) / 2;
     const size_t smem = (size_t)npair * B * 33 * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_ramp_reg<B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        attr = true;
-    }
+    static SmemAttr attr;
+    cudaError_t e = ensure_smem((const void*)k_ramp_reg<B>, (int)smem, attr);
+    if (e != cudaSuccess) return e;
     const int nchunk = (Nch + Kc - 1) / Kc;
     dim3 grid(g.Nv, ns * nchunk);
     k_ramp_reg<B><<<grid, 32 * npair, smem, s>>>(in, ld_in, Nch, g.Nv, g.Nr, g.Nc, s0, ns, t.Hhat, t.twiddle, Q,
@@ -503,11 +501,9 @@ cudaError_t ramp_filter(const Geometry& g, const DeviceTables& t, const float* i
     }
     const int npair = (std::min(Nch, Kc) + 1) / 2;
     const size_t smem = (size_t)npair * g.P * sizeof(float2);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_ramp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    static SmemAttr attr;
+    cudaError_t e = ensure_smem((const void*)k_ramp, (int)smem, attr);
+    if (e != cudaSuccess) return e;
     const int nchunk = (Nch + Kc - 1) / Kc;
     dim3 grid(g.Nv, ns * nchunk);
     k_ramp<<<grid, RT, smem, s>>>(in, ld_in, Nch, g.Nv, g.Nr, g.Nc, g.P, g.logP, s0, ns, t.Hhat, t.twiddle,
@@ -523,11 +519,9 @@ static cudaError_t bp_kv(const Geometry& g, const DeviceTables& t, const float* 
     const int per_view = bp_wmax(VPT) * bp_pitch(KC) * (int)sizeof(float);
     const int vch = std::max(1, std::min(std::min(g.Nv, BVMAX), ((KC <= 8 ? 20 : 40) * 1024) / per_view));
     const size_t smem = (size_t)2 * vch * per_view;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_backproject<KC, VPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        attr = true;
-    }
+    static SmemAttr attr;
+    cudaError_t e = ensure_smem((const void*)k_backproject<KC, VPT>, (int)smem, attr);
+    if (e != cudaSuccess) return e;
     const int nchunk = (Nch + KC - 1) / KC;
     dim3 grid((g.Nc + BTX - 1) / BTX, (g.Nc + 16 * VPT - 1) / (16 * VPT), ns * nchunk);
     k_backproject<KC, VPT><<<grid, BTX * 16, smem, s>>>(Q, Nch, g.Nv, g.Nc, s0, ns, t.cos_t, t.sin_t, mode, out,

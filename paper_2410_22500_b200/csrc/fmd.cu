@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(FT, 2) k_fmd_tpart(const float* __restrict__ X
     unsigned bad = 0;
     for (int64_t n = n0 + tid; n < n1; n += FT) {
         const int lab = labels[n];
-        if (lab >= Nm) bad = ST_INIT_BAD;
+        if (lab >= Nm || lab < -1) bad = ST_LABEL_BAD;
         const int rr = lab - i0;
         if (rr < 0 || rr >= nr) continue;
         float x[K];
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(FT, 2) k_fmd_tpart(const float* __restrict__ X
     }
 }
 
-// T = (sum over blocks, fixed order) / count; an empty region flags ST_Y_ALLZERO (E_DATA).
+// T = (sum over blocks, fixed order) / count; an empty region flags ST_REGION_EMPTY (E_DATA).
 __global__ void __launch_bounds__(FT) k_fmd_tfinal(const double* __restrict__ part, const long long* __restrict__ cnt,
                                                    int nblk, int Nm, int K, float* __restrict__ T,
                                                    unsigned* __restrict__ status) {
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(FT) k_fmd_tfinal(const double* __restrict__ pa
             c += cnt[(int64_t)b * FMD_MAXM + i];
         }
         if (c == 0) {
-            atomicOr(status, (unsigned)ST_Y_ALLZERO);
+            atomicOr(status, (unsigned)ST_REGION_EMPTY);
             T[o] = 0.f;
         } else {
             T[o] = (float)(s / (double)c);

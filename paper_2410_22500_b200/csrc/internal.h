@@ -5,9 +5,32 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 namespace hsnct {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: a kernel's attribute is
+// raised on the calling thread's current device the first time a launch there needs more
+// than 48 KB, and remembered per device (atomic; a race only repeats the call).
+constexpr int MAX_DEVICES = 64;
+struct SmemAttr {
+    std::atomic<int> bytes[MAX_DEVICES] = {};
+};
+inline cudaError_t ensure_smem(const void* func, int bytes, SmemAttr& a) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < MAX_DEVICES && a.bytes[dev].load(std::memory_order_acquire) >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < MAX_DEVICES) {
+        int cur = a.bytes[dev].load(std::memory_order_relaxed);
+        while (cur < bytes && !a.bytes[dev].compare_exchange_weak(cur, bytes, std::memory_order_release)) {
+        }
+    }
+    return cudaSuccess;
+}
 
 // Device status word bits (deferred errors, read back by hsnct_sync).
 enum : unsigned {
@@ -15,6 +38,8 @@ enum : unsigned {
     ST_Y_ALLZERO = 2u,       // E_DATA
     ST_INIT_BAD = 4u,        // E_DATA: V0/D0 non-finite or negative
     ST_NUMERIC = 8u,         // E_NUMERIC: V or D became non-finite
+    ST_LABEL_BAD = 16u,      // E_DATA: an FMD label outside [-1, n_mat)
+    ST_REGION_EMPTY = 32u,   // E_DATA: an FMD user region has no voxel
 };
 
 struct Geometry {
@@ -45,6 +70,7 @@ struct NmfPlan {
     // fused single-pass path (nmf_fused.cu), K <= 8
     bool fused;
     bool persist;    // run all iterations in one cooperative launch (fused path)
+    bool persist_fits;  // the persistent kernel's lambda slice fits its D-update buffers
     int LP;          // lambda pairs per thread
     int nbuf;        // ring slots per compute group
     int ngrp;        // compute groups of 4 warps (3 or 4)
@@ -55,12 +81,6 @@ struct NmfPlan {
     int fthreads;    // threads per CTA
     int nblk_f;      // CTAs (persistent, static tile schedule)
     size_t smem_f;   // dynamic smem (tile ring)
-    // tensor-core path (nmf_mma.cuh), K <= 8, persistent only
-    bool mma;
-    int N16;         // Nk rounded up to 16
-    int spw;         // k-steps per warp
-    int nslot;       // tile slots
-    size_t smem_m;   // dynamic smem
     // two-pass fallback (nmf.cu)
     int nblk_v, nchunk, bthreads, nlam_blk;
     int64_t rows_per_chunk;
@@ -104,13 +124,8 @@ cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs&
                                double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                              unsigned* status, cudaStream_t s);
-// tensor-core path: plan, Y+ hi/lo split, all iterations in one cooperative launch
-bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p);
-cudaError_t nmf_ysplit_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
-                              unsigned* status, cudaStream_t s);
-cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
-                           double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
+std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p);
 // counter words needed by the handle: 1 + ceil(Nk / 32)
 
 // ------------------------------------------------------------- FBP (fbp.cu)

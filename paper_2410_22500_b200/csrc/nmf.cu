@@ -11,6 +11,7 @@
 // Everything is deterministic: static schedules, fixed-order reductions, no
 // floating-point atomics (the only atomics are integer status / ticket words).
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -521,16 +522,7 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.nbx = (g.Nk + 31) / 32;
     p.fused = nmf_fused_plan(g, num_sms, &p);
     const char* np_env = getenv("HSNCT_NO_PERSIST");
-    p.persist = p.fused && !(np_env && np_env[0] == '1');
-    // the tensor-core path is persistent-only; its grid equals the fused path's
-    NmfPlan q = p;
-    p.mma = p.persist && nmf_mma_plan(g, num_sms, &q);
-    if (p.mma) {
-        p.N16 = q.N16;
-        p.spw = q.spw;
-        p.nslot = q.nslot;
-        p.smem_m = q.smem_m;
-    }
+    p.persist = p.fused && p.persist_fits && !(np_env && np_env[0] == '1');
     // two-pass fallback (K > 8 or very long spectra)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
@@ -560,7 +552,7 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     b += align256((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));   // Gpart
     b += align256(sizeof(double));                                    // ysq
     b += align256((size_t)p.PH * KK * sizeof(double));                // Hpart
-    const size_t bstride = std::max<size_t>(p.Nkp, p.mma ? p.N16 : 0);
+    const size_t bstride = p.Nkp;
     b += align256((size_t)p.P * g.K * bstride * sizeof(float));       // Bpart
     b += align256((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));   // L2B
     b += align256((size_t)p.nbx * DG2 * KK * sizeof(double));         // L2H
@@ -586,7 +578,7 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
     w.Gpart = (double*)take((size_t)std::max(p.nbx, p.nblk_f) * KK * sizeof(double));
     w.ysq = (double*)take(sizeof(double));
     w.Hpart = (double*)take((size_t)p.PH * KK * sizeof(double));
-    const size_t bstride = std::max<size_t>(p.Nkp, p.mma ? p.N16 : 0);
+    const size_t bstride = p.Nkp;
     w.Bpart = (float*)take((size_t)p.P * g.K * bstride * sizeof(float));
     w.L2B = (double*)take((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));
     w.L2H = (double*)take((size_t)p.nbx * DG2 * KK * sizeof(double));
@@ -601,10 +593,7 @@ int nmf_init_launches(const NmfPlan& p) { return p.fused ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s) {
-    if (p.mma) {
-        cudaError_t e = nmf_ysplit_launch(g, p, w, Y, ld_y, status, s);
-        if (e != cudaSuccess) return e;
-    } else if (p.fused) {
+    if (p.fused) {
         cudaError_t e = nmf_yplus_launch(g, p, w, Y, ld_y, status, s);
         if (e != cudaSuccess) return e;
     }
@@ -631,12 +620,10 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
         cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
     } else {
-        static bool attr_done = false;  // per-K instantiation
-        if (!attr_done) {
-            cudaFuncSetAttribute(k_vstep<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            cudaFuncSetAttribute(k_vstep<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            attr_done = true;
-        }
+        static SmemAttr attr_f, attr_n;  // per K instantiation, per device
+        cudaError_t e = first ? ensure_smem((const void*)k_vstep<K, true>, (int)p.smem_v, attr_f)
+                              : ensure_smem((const void*)k_vstep<K, false>, (int)p.smem_v, attr_n);
+        if (e != cudaSuccess) return e;
         if (first)
             k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
         else
@@ -653,6 +640,19 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
 }
 
 int nmf_launches_per_iter(const NmfPlan& p) { return p.fused ? 2 : 3; }
+
+std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
+    char b[256];
+    if (p.persist)
+        snprintf(b, sizeof b, "persist k_nmf_persist<K=%d,LP=%d,NBG=%d,NGRP=%d> grid=%d", g.K, p.LP, p.nbuf,
+                 p.ngrp, p.nblk_f);
+    else if (p.fused)
+        snprintf(b, sizeof b, "fused k_nmf_fused<K=%d,LP=%d,NBG=%d,NGRP=%d>+k_dred grid=%d", g.K, p.LP, p.nbuf,
+                 p.ngrp, p.nblk_f);
+    else
+        snprintf(b, sizeof b, "twopass k_vstep<K=%d>+k_bpart+k_dred grid=%d", g.K, p.nblk_v);
+    return b;
+}
 
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,
                             int64_t ld_y, float* V, float* D, int it, double* obj2,

@@ -40,6 +40,12 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int64_t ntiles = (Np + RG - 1) / RG;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));
     p->PB = p->nblk_f;
+    // the persistent kernel's D update gives every CTA a lambda slice of SL = ceil(Nk / nCTA)
+    // bins: dnew holds 64 per component, the fp64 B slice SCR/2 values, and threads
+    // [0, K*K + K*SL) produce its outputs.  Shapes beyond that (few rows, long spectra) run
+    // the per-iteration launches (k_nmf_fused + k_dred) instead.
+    const int SL = (g.Nk + p->nblk_f - 1) / p->nblk_f;
+    p->persist_fits = SL <= 64 && g.K * SL <= SCR / 2 && g.K * g.K + g.K * SL <= p->fthreads;
     p->nby = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (Np + 7) / 8));
     return true;
 }

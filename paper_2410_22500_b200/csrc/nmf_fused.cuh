@@ -943,13 +943,9 @@ inline size_t fused_smem_bytes(int Nkp, int K, int LP, int NBG, int NGRP) {
 template <int K, int LP, int NB, int NG>
 inline cudaError_t fused_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
                              int it, unsigned* status, cudaStream_t s) {
-    static size_t attr = 0;  // dynamic smem the kernel is currently allowed (static + dynamic <= 227 KB)
-    if (attr < p.smem_f) {
-        cudaError_t e = cudaFuncSetAttribute(k_nmf_fused<K, LP, NB, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)p.smem_f);
-        if (e != cudaSuccess) return e;
-        attr = p.smem_f;
-    }
+    static SmemAttr attr;  // dynamic smem the kernel is allowed, per device (static + dynamic <= 227 KB)
+    cudaError_t e = ensure_smem((const void*)k_nmf_fused<K, LP, NB, NG>, (int)p.smem_f, attr);
+    if (e != cudaSuccess) return e;
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     k_nmf_fused<K, LP, NB, NG><<<p.nblk_f, NG * TG, p.smem_f, s>>>(w.Yp, Np, g.Nk, p.Nkp, V, D, w.Gd, w.Bpart,
                                                                   w.Hpart, w.vpart, it, (p.rotate ? 1 : 0) | (p.l2pf ? 2 : 0), status);
@@ -959,13 +955,9 @@ inline cudaError_t fused_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w
 template <int K, int LP, int NB, int NG>
 inline cudaError_t persist_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D,
                                int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
-    static size_t attr = 0;
-    if (attr < p.smem_f) {
-        cudaError_t e = cudaFuncSetAttribute(k_nmf_persist<K, LP, NB, NG>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem_f);
-        if (e != cudaSuccess) return e;
-        attr = p.smem_f;
-    }
+    static SmemAttr attr;
+    cudaError_t e0 = ensure_smem((const void*)k_nmf_persist<K, LP, NB, NG>, (int)p.smem_f, attr);
+    if (e0 != cudaSuccess) return e0;
     PersistArgs A;
     A.Yp = w.Yp;
     A.Np = (int64_t)g.Nv * g.Nr * g.Nc;

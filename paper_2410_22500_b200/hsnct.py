@@ -21,6 +21,9 @@ OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
 OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD = range(5)
 MAX_SUB = 16
 
+# hsnct_window_fn: void (*)(void* user, int slice0, int n_slices, const float* xh)
+WINDOW_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p)
+
 _lock = threading.Lock()
 _lib = None
 
@@ -63,6 +66,10 @@ def lib():
             L.hsnct_dhr.restype = i32
             L.hsnct_fhr_host.argtypes = [vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, sz, vp]
             L.hsnct_fhr_host.restype = i32
+            L.hsnct_fhr_stream_bytes.argtypes = [vp, i32]
+            L.hsnct_fhr_stream_bytes.restype = sz
+            L.hsnct_fhr_stream.argtypes = [vp, vp, i64, vp, vp, i32, i32, vp, WINDOW_FN, vp, vp, vp, vp, sz, vp]
+            L.hsnct_fhr_stream.restype = i32
             L.hsnct_sync.argtypes = [vp, vp]
             L.hsnct_sync.restype = i32
             L.hsnct_kernel_launches.argtypes = [vp]
@@ -79,6 +86,8 @@ def lib():
             L.hsnct_fmd_spectra.restype = i32
             L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
             L.hsnct_debug_trace.restype = i32
+            L.hsnct_debug_plan.argtypes = [vp, ctypes.c_char_p, sz]
+            L.hsnct_debug_plan.restype = i32
             L.hsnct_debug_fbp_timing.argtypes = [vp, ctypes.c_int]
             L.hsnct_debug_fbp_timing.restype = i32
             L.hsnct_debug_fbp_times.argtypes = [vp, vp]
@@ -154,6 +163,10 @@ class Hsnct:
             ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
             self._ws[op] = ws
         return ws
+
+    def release_workspaces(self):
+        """Drop the workspaces this handle cached (their device memory returns to torch)."""
+        self._ws.clear()
 
     # -- checks ---------------------------------------------------------------------
     def _dev(self, t, name, shape=None, contiguous=True):
@@ -244,6 +257,57 @@ class Hsnct:
                                     _stream(stream, self.device)))
         return Xh
 
+    def fhr_stream_window_slices(self, budget_bytes: int = 2 << 30) -> int:
+        """Default x^h window (slices) of fhr_stream: the largest that fits budget_bytes."""
+        per = self.Nc * self.Nc * self.Nk * 4
+        return max(1, min(self.Nr, budget_bytes // per))
+
+    def fhr_stream_ring(self, window_slices: int) -> torch.Tensor:
+        """A page-locked host ring of two x^h windows for fhr_stream."""
+        return torch.empty((2, window_slices * self.Nc * self.Nc, self.Nk), dtype=torch.float32, pin_memory=True)
+
+    def fhr_stream(self, Y, V0, D0, n_iter, window_slices=None, ring=None, on_window=None, V=None, D=None,
+                   ws=None, stream=None):
+        """Algorithm 1 end to end on HOST tensors with x^h streamed out in windows
+        (hsnct_fhr_stream).  on_window(slice0, n_slices, xh) is called on this thread for every
+        window as soon as it is on the host; xh is a [n_slices*N_c*N_c, N_k] view into the ring,
+        valid only during the call.  Blocks until the last window has been delivered."""
+        for t, name in ((Y, "Y"), (V0, "V0"), (D0, "D0")):
+            if t.device.type != "cpu" or t.dtype != torch.float32:
+                raise HsnctError(E_ARG, f"{name} must be a float32 host tensor")
+        if Y.dim() != 2 or Y.shape != (self.Np, self.Nk) or Y.stride(1) != 1:
+            raise HsnctError(E_ARG, "Y must be [N_p, N_k] with unit column stride")
+        V0 = V0.contiguous()
+        D0 = D0.contiguous()
+        wsl = self.fhr_stream_window_slices() if window_slices is None else int(window_slices)
+        wsl = max(1, min(wsl, self.Nr))
+        if ring is None:
+            ring = self.fhr_stream_ring(wsl)
+        if not ring.is_contiguous() or ring.numel() < 2 * wsl * self.Nc * self.Nc * self.Nk or ring.device.type != "cpu":
+            raise HsnctError(E_ARG, "ring must be a contiguous host tensor of two windows")
+        if ws is None:
+            ws = torch.empty(lib().hsnct_fhr_stream_bytes(self._h, wsl), dtype=torch.uint8, device=self.device)
+        per = self.Nc * self.Nc * self.Nk
+        base = ring.data_ptr()
+        flat = ring.reshape(-1)
+        err = []
+
+        def cb(_user, s0, ns, ptr):
+            try:
+                if on_window is not None:
+                    off = (ptr - base) // 4
+                    on_window(s0, ns, flat[off:off + ns * per].view(ns * self.Nc * self.Nc, self.Nk))
+            except BaseException as e:  # noqa: BLE001 -- re-raised after the C call returns
+                err.append(e)
+
+        fn = WINDOW_FN(cb)
+        _check(lib().hsnct_fhr_stream(self._h, _ptr(Y), Y.stride(0), _ptr(V0), _ptr(D0), int(n_iter), wsl,
+                                      _ptr(ring), fn, None, _ptr(V), _ptr(D), _ptr(ws),
+                                      ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        if err:
+            raise err[0]
+        return ring
+
     # -- FMD back half (NEXT-2; Algorithm 2, PAPER.md:333-373) ---------------------------
     def fmd_transform(self, X, labels, n_mat, T=None, ws=None, stream=None):
         """Eq. 7: T [n_mat, K] region means of X [K, N_r, N_c, N_c] (hsnct_fmd_transform)."""
@@ -282,6 +346,12 @@ class Hsnct:
         self._dev(Dm, "Dm", (n_mat, self.Nk))
         _check(lib().hsnct_fmd_spectra(self._h, _ptr(D), _ptr(T), int(n_mat), _ptr(Dm), _stream(stream, self.device)))
         return Dm
+
+    def debug_plan(self) -> str:
+        """The subspace-extraction plan (row-pass kernel, template, grid) chosen at create."""
+        buf = ctypes.create_string_buffer(256)
+        _check(lib().hsnct_debug_plan(self._h, buf, 256))
+        return buf.value.decode()
 
     def debug_fbp_timing(self, on: bool):
         """Record CUDA events around the ramp filter and backprojection of later fbp calls."""

@@ -68,6 +68,9 @@ CONFIGS = {
     3: Config(3, 256, 64, 120, 1600, 5, 200, 5, 30.0, False),
     4: Config(4, 512, 128, 64, 1600, 6, 300, 6, 20.0, True),
     5: Config(5, 512, 256, 64, 1600, 6, 300, 6, 20.0, True),
+    # not in BASELINE.json: the paper's Table I simulated-data shape:
+    # 512 x 512 detector, N_r = 512 slices, N_v = 32 views, N_k = 1200, N_s = 9 (K > 8)
+    6: Config(6, 512, 512, 32, 1200, 9, 300, 3, 20.0, False),
 }
 
 
@@ -252,8 +255,20 @@ def log_table() -> np.ndarray:
     return np.log(np.maximum(n, 0.5))
 
 
+def expected_counts(ptrue: torch.Tensor, counts: float) -> torch.Tensor:
+    """Mean transmitted counts C exp(-p) (Eq. 10 without noise), fp64."""
+    return counts * torch.exp(-ptrue)
+
+
+def neglog(y0: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """Eq. 2 on (possibly real-valued) counts with the 1/2-count floor (R7):
+    ln(max(y0, 1/2)) - ln(max(y, 1/2)), fp64.  The integer-count path in make_problem uses the
+    same function through the 256-entry table log_table()."""
+    return torch.log(torch.clamp(y0.double(), min=0.5)) - torch.log(torch.clamp(y.double(), min=0.5))
+
+
 def make_problem(cfg: Config, device="cpu", noise: bool = True, chunk_rows: int = 1 << 18,
-                 dtype_y=torch.float32):
+                 dtype_y=torch.float32, return_counts: bool = False):
     """Draw (Y, V0, D0) for a config.  Returns a dict:
 
     Y   [Np, Nk] fp32, -log transmission (Eq. 2), row p = (v Nr + r) Nc + c.
@@ -261,6 +276,8 @@ def make_problem(cfg: Config, device="cpu", noise: bool = True, chunk_rows: int 
     P   [M, Nv, Nr, Nc] fp64 material sinograms, mu [M, Nk] fp64 spectra (scaled),
     shapes, angles, plus the config.
     With noise=False, Y = fp32(p_true): exactly rank M in fp64 before the cast.
+    return_counts=True adds the uint8 counts: y0 [Nr*Nc, Nk] (open beam, shared by all
+    views) and y [Np, Nk], with Y[p] = fp32(L[y0[p % (Nr*Nc)]] - L[y[p]]) (noise=True only).
     """
     dev = torch.device(device)
     shapes = make_phantom(cfg)
@@ -282,19 +299,26 @@ def make_problem(cfg: Config, device="cpu", noise: bool = True, chunk_rows: int 
                                       dtype=torch.float64, device=dev), generator=g)
         assert float(ob.max()) <= 255.0
         Lob = L[ob.long()]
+        if return_counts:
+            y_all = torch.empty((cfg.Np, cfg.Nk), dtype=torch.uint8, device=dev)
     for p0 in range(0, cfg.Np, chunk_rows):
         p1 = min(cfg.Np, p0 + chunk_rows)
         ptrue = Pm[p0:p1] @ mu_t                                      # Eq. 3, w = 0
         if noise:
-            y = torch.poisson(cfg.counts * torch.exp(-ptrue), generator=g)   # Eq. 10 + Poisson
+            y = torch.poisson(expected_counts(ptrue, cfg.counts), generator=g)   # Eq. 10 + Poisson
             assert float(y.max()) <= 255.0
+            if return_counts:
+                y_all[p0:p1] = y.to(torch.uint8)
             rc = torch.arange(p0, p1, device=dev) % (cfg.Nr * cfg.Nc)
             Y[p0:p1] = (Lob[rc] - L[y.long()]).to(dtype_y)            # Eq. 2 via the log table
         else:
             Y[p0:p1] = ptrue.to(dtype_y)
     V0, D0 = make_init(Y, cfg.K, seeds(cfg)["init"])
-    return dict(cfg=cfg, Y=Y, V0=V0, D0=D0, P=P, mu=mu, shapes=shapes,
-                angles=view_angles(cfg.Nv))
+    out = dict(cfg=cfg, Y=Y, V0=V0, D0=D0, P=P, mu=mu, shapes=shapes, angles=view_angles(cfg.Nv))
+    if return_counts and noise:
+        out["y0"] = ob.to(torch.uint8)
+        out["y"] = y_all
+    return out
 
 
 def make_init(Y: torch.Tensor, K: int, seed: int):

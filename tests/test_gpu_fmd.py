@@ -94,13 +94,18 @@ def test_fmd_errors():
     h.fmd_transform(X, lab, 2)                  # region 1 is empty -> deferred data error
     with pytest.raises(HsnctError) as e:
         h.sync()
-    assert e.value.status == 2
+    assert e.value.status == 2 and "region is empty" in str(e.value)
     lab[0] = 5                                  # label >= n_mat -> deferred data error
     lab[1] = 1
     h.fmd_transform(X, lab, 2)
     with pytest.raises(HsnctError) as e:
         h.sync()
-    assert e.value.status == 2
+    assert e.value.status == 2 and "label outside" in str(e.value)
+    lab[0] = -3                                 # labels < -1 are not "none": data error
+    h.fmd_transform(X, lab, 2)
+    with pytest.raises(HsnctError) as e:
+        h.sync()
+    assert e.value.status == 2 and "label outside" in str(e.value)
 
 
 def test_fmd_nnls_random_supports():

@@ -106,23 +106,6 @@ def test_nmf_deterministic_and_resumable(H):
 
 @pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
                                         (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
-def test_nmf_mma_path(H, monkeypatch, cfg, n_iter):
-    """The opt-in tensor-core (mma.sync, fp16 hi/lo split) persistent kernel."""
-    monkeypatch.setenv("HSNCT_MMA", "1")
-    pr = sd.make_problem(cfg)
-    h = H(cfg)
-    V = pr["V0"].to(DEV).clone()
-    D = pr["D0"].to(DEV).clone()
-    obj = torch.zeros(2 * n_iter, dtype=torch.float64, device=DEV)
-    h.subspace_decompose(padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4), V, D, n_iter, obj_trace=obj)
-    h.sync()
-    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter, objective=True)
-    assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
-    np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
-
-
-@pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
-                                        (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
 def test_nmf_per_iteration_fallback(H, monkeypatch, cfg, n_iter):
     """The per-iteration launch path (used when a cooperative launch is refused)."""
     monkeypatch.setenv("HSNCT_NO_PERSIST", "1")
@@ -372,6 +355,33 @@ def test_fhr_host_matches_device_path(H):
     h.sync()
     assert torch.equal(Vh, V.cpu()) and torch.equal(Dh, D.cpu())
     assert torch.equal(Xh_host, Xh.cpu())
+
+
+@pytest.mark.parametrize("wsl", [1, 2, 5])
+def test_fhr_stream_windows_match_device_path(H, wsl):
+    """hsnct_fhr_stream: every x^h window is delivered once, in order, and equals the device
+    path bit for bit (same kernels on the same inputs); ragged last window (5 slices)."""
+    cfg = sd.custom(idx=41, Nc=24, Nv=12, Nr=5, Nk=70, K=3, M=3)
+    pr = sd.make_problem(cfg)
+    h = H(cfg)
+    n = 15
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(pr["Y"].to(DEV), V, D, n)
+    Xh = h.synthesize(h.fbp(V), D)
+    h.sync()
+    Xh = Xh.cpu()
+    got = []
+    per = cfg.Nc * cfg.Nc
+
+    def on_window(s0, ns, xh):
+        got.append((s0, ns))
+        assert torch.equal(xh, Xh[s0 * per:(s0 + ns) * per])
+
+    Vh = torch.empty_like(pr["V0"])
+    h.fhr_stream(pr["Y"].pin_memory(), pr["V0"], pr["D0"], n, window_slices=wsl, on_window=on_window, V=Vh)
+    assert got == [(s, min(wsl, cfg.Nr - s)) for s in range(0, cfg.Nr, wsl)]
+    assert torch.equal(Vh, V.cpu())
 
 
 # ----------------------------------------------------------------- errors
