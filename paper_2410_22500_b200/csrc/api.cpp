@@ -74,6 +74,8 @@ struct DeviceGuard {
 
 size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
 
+int trace_ctas(const NmfPlan& p) { return p.tc ? TC_CLUSTER * p.tc_ncl : p.nblk_f; }
+
 bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
 
 struct Range {
@@ -336,9 +338,9 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     if (e == cudaSuccess) e = cudaMemset(h->t.status, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
     const char* tr = getenv("HSNCT_TRACE");
-    if (e == cudaSuccess && tr && tr[0] == '1' && h->nmf.persist) {
+    if (e == cudaSuccess && tr && tr[0] == '1' && (h->nmf.persist || h->nmf.tc)) {
         h->trace_iters = 256;
-        const size_t tb = (size_t)h->trace_iters * h->nmf.nblk_f * TRACE_SLOTS * sizeof(uint64_t);
+        const size_t tb = (size_t)h->trace_iters * trace_ctas(h->nmf) * TRACE_SLOTS * sizeof(uint64_t);
         e = cudaMalloc((void**)&h->trace, tb);
         if (e == cudaSuccess) e = cudaMemset(h->trace, 0, tb);
     }
@@ -711,10 +713,10 @@ uint64_t hsnct_kernel_launches(hsnct_t h) { return h ? h->launches : 0; }
 hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta) {
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "debug_trace: handle is NULL");
-    const size_t avail = h->trace ? (size_t)h->trace_iters * h->nmf.nblk_f * TRACE_SLOTS : 0;
+    const size_t avail = h->trace ? (size_t)h->trace_iters * trace_ctas(h->nmf) * TRACE_SLOTS : 0;
     const size_t m = std::min(n, avail);
     if (n_out) *n_out = avail;
-    if (n_cta) *n_cta = h->nmf.nblk_f;
+    if (n_cta) *n_cta = trace_ctas(h->nmf);
     if (m == 0) return HSNCT_OK;
     if (!host) return fail(HSNCT_E_ARG, "debug_trace: host buffer is NULL");
     DeviceGuard guard(h->device);

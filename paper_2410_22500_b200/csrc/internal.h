@@ -61,6 +61,13 @@ struct DeviceTables {
 
 // ---------------------------------------------------------------- NMF (nmf.cu)
 constexpr int DG2 = 8;  // chunk groups of the D-update reduction
+constexpr int TC_CLUSTER = 4;  // CTAs per cluster of the tcgen05 row pass (bin ranges)
+struct TcRanges {
+    int l0[TC_CLUSTER];   // first bin of cluster rank j's range (multiple of 16)
+    int L[TC_CLUSTER];    // bins in the range (multiple of 16)
+    int nch[TC_CLUSTER];  // chunks of W bins in the range (the last one may be shorter)
+    int W;                // chunk width in bins (multiple of 16, <= 128)
+};
 struct NmfPlan {
     int Nkp;         // Nk rounded up to 4
     int nbx;         // D-update column blocks = ceil(Nk / 32)
@@ -81,6 +88,16 @@ struct NmfPlan {
     int fthreads;    // threads per CTA
     int nblk_f;      // CTAs (persistent, static tile schedule)
     size_t smem_f;   // dynamic smem (tile ring)
+    // tcgen05 row pass (nmf_tc.cu), K <= 8: one launch per iteration + k_dred
+    bool tc;
+    int tc_ncl;      // clusters (TC_CLUSTER CTAs each)
+    int tc_R;        // ring slots per CTA
+    int tc_R2;       // phase-2 ring slots (0: phase 2 reads the phase-1 ring)
+    int tc_maxch;    // chunks of the longest bin range
+    size_t tc_smem;  // dynamic smem
+    TcRanges tc_rg;
+    int tc_Nk16;     // Nk rounded up to 16
+    int64_t tc_Npad; // Np rounded up to the 64-row tile
     // two-pass fallback (nmf.cu)
     int nblk_v, nchunk, bthreads, nlam_blk;
     int64_t rows_per_chunk;
@@ -97,13 +114,16 @@ struct NmfWs {
     double* L2B;     // [nbx*DG2*K*32]
     double* L2H;     // [nbx*DG2*K*K]
     float* Yp;       // [Np*Nkp] Y+ (fused path only)
-    double* ypart;   // [nby] ||Y+||^2 partials (fused path only)
+    double* ypart;   // [nby] ||Y+||^2 partials (fused and tc paths)
+    void* Yc;        // [Npad*Nk16] Y+ as fp16 hi/lo pairs in the tcgen05 layout (tc path)
+    unsigned* ymax;  // bits of max(Y+) (tc path)
     // diagnostics (hsnct_debug_trace): per-iteration, per-CTA %globaltimer stamps
     uint64_t* trace = nullptr;  // [trace_iters][nCTA][TRACE_SLOTS] or null
     int trace_iters = 0;
 };
-constexpr int TRACE_SLOTS = 8;   // iteration start, pass end, barrier 1, D update done, iteration end,
-                                 // partials reduced, D slice updated, G reduced + D restaged
+constexpr int TRACE_SLOTS = 16;  // persist: [iteration][CTA] iteration start, pass end, barrier 1, D update
+                                 // done, iteration end, partials reduced, D slice updated, G reduced +
+                                 // D restaged; tc: [tile][CTA] (nmf_tc.cu, TcStamp)
 NmfPlan nmf_plan(const Geometry& g, int num_sms);
 bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p);
 size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);
@@ -124,6 +144,13 @@ cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs&
                                double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                              unsigned* status, cudaStream_t s);
+// tcgen05 path: plan (fills the tc_* fields), input preparation (max / ||Y+||^2 / non-finite
+// check, then the fp16 hi/lo conversion), one row pass
+bool nmf_tc_plan(const Geometry& g, int num_sms, NmfPlan* p);
+cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                           unsigned* status, cudaStream_t s);
+cudaError_t nmf_tc_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
+                          unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
 std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p);
 // counter words needed by the handle: 1 + ceil(Nk / 32)

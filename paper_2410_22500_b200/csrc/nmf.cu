@@ -11,8 +11,10 @@
 // Everything is deterministic: static schedules, fixed-order reductions, no
 // floating-point atomics (the only atomics are integer status / ticket words).
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "internal.h"
 
@@ -24,6 +26,9 @@ constexpr int VW = VT / 32;    // row-pass warps
 constexpr int RPW = 4;         // rows per warp step
 constexpr int BT_MAX = 128;    // column-pass threads (one lambda quad each)
 constexpr int BROWS = 32;      // V rows staged per column-pass sub-chunk
+// default plan: the FFMA row pass everywhere -- the tcgen05 pass measured 0.53 of HBM at
+// C3 / C5 against the persistent FFMA kernel's 0.72 (profiles/r02/tc/)
+constexpr int64_t TC_MIN_ROWS = INT64_MAX;
 
 __device__ __forceinline__ float4 ld4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
@@ -523,6 +528,21 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.fused = nmf_fused_plan(g, num_sms, &p);
     const char* np_env = getenv("HSNCT_NO_PERSIST");
     p.persist = p.fused && p.persist_fits && !(np_env && np_env[0] == '1');
+    // tcgen05 row pass: HSNCT_NMF=tc / ffma forces the choice; by default the plan takes the
+    // kernel that measured faster on the shape (TC_MIN_ROWS)
+    {
+        const char* nm = getenv("HSNCT_NMF");
+        const bool force_tc = nm && strcmp(nm, "tc") == 0, force_ffma = nm && strcmp(nm, "ffma") == 0;
+        const bool want = force_tc || (!force_ffma && Np >= TC_MIN_ROWS);
+        NmfPlan q = p;
+        if (want && nmf_tc_plan(g, num_sms, &q)) {
+            p = q;
+            p.tc = true;
+            p.fused = false;
+            p.persist = false;
+            p.nby = num_sms * 8;
+        }
+    }
     // two-pass fallback (K > 8 or very long spectra)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
@@ -537,9 +557,9 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.rows_per_chunk = (Np + p.nchunk - 1) / p.nchunk;
     p.nchunk = (int)((Np + p.rows_per_chunk - 1) / p.rows_per_chunk);
     if (p.nchunk < 1) p.nchunk = 1;
-    p.P = p.fused ? p.PB : p.nchunk;
-    p.PH = p.fused ? p.PB : p.nchunk;
-    p.nvp = p.fused ? p.PB : p.nblk_v;
+    p.P = p.tc ? p.tc_ncl : p.fused ? p.PB : p.nchunk;
+    p.PH = p.tc ? TC_CLUSTER * p.tc_ncl : p.fused ? p.PB : p.nchunk;
+    p.nvp = p.tc ? TC_CLUSTER * p.tc_ncl : p.fused ? p.PB : p.nblk_v;
     return p;
 }
 
@@ -557,8 +577,13 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     b += align256((size_t)p.nbx * DG2 * g.K * 32 * sizeof(double));   // L2B
     b += align256((size_t)p.nbx * DG2 * KK * sizeof(double));         // L2H
     if (p.fused) {
-        b += align256((size_t)Np_(g) * bstride * sizeof(float));      // Yp (fp32) or Y+ hi/lo halves
+        b += align256((size_t)Np_(g) * bstride * sizeof(float));      // Yp (fp32)
         b += align256((size_t)p.nby * sizeof(double));                // ypart
+    }
+    if (p.tc) {
+        b += align256((size_t)p.tc_Npad * p.tc_Nk16 * 4);             // Yc: fp16 hi + lo per element
+        b += align256((size_t)p.nby * sizeof(double));                // ypart
+        b += align256(2 * sizeof(unsigned));                          // ymax, max row norm
     }
     return b;
 }
@@ -586,14 +611,22 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
         w.Yp = (float*)take((size_t)Np_(g) * bstride * sizeof(float));
         w.ypart = (double*)take((size_t)p.nby * sizeof(double));
     }
+    if (p.tc) {
+        w.Yc = take((size_t)p.tc_Npad * p.tc_Nk16 * 4);
+        w.ypart = (double*)take((size_t)p.nby * sizeof(double));
+        w.ymax = (unsigned*)take(2 * sizeof(unsigned));
+    }
     return w;
 }
 
-int nmf_init_launches(const NmfPlan& p) { return p.fused ? 2 : 1; }
+int nmf_init_launches(const NmfPlan& p) { return p.tc ? 3 : p.fused ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s) {
-    if (p.fused) {
+    if (p.tc) {
+        cudaError_t e = nmf_tc_prepare(g, p, w, Y, ld_y, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.fused) {
         cudaError_t e = nmf_yplus_launch(g, p, w, Y, ld_y, status, s);
         if (e != cudaSuccess) return e;
     }
@@ -616,7 +649,10 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
                           unsigned* status, unsigned* counter, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const bool first = it == 0;
-    if (p.fused) {
+    if (p.tc) {
+        cudaError_t e = nmf_tc_launch(g, p, w, V, D, it, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.fused) {
         cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
     } else {
@@ -633,17 +669,21 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
     }
     dim3 gd(p.nbx, DG2);
     k_dred<K><<<gd, 256, 0, s>>>(w.Bpart, w.Hpart, p.P, p.PH, g.Nk, p.Nkp, D, w.Gd, w.vpart, p.nvp,
-                                 w.ypart, p.fused ? p.nby : 0, w.L2B,
+                                 w.ypart, (p.fused || p.tc) ? p.nby : 0, w.L2B,
                                  w.L2H, w.dpart, w.Gpart, w.ysq, first ? 1 : 0, obj2, counter + 1,
                                  counter, status);
     return cudaGetLastError();
 }
 
-int nmf_launches_per_iter(const NmfPlan& p) { return p.fused ? 2 : 3; }
+int nmf_launches_per_iter(const NmfPlan& p) { return (p.fused || p.tc) ? 2 : 3; }
 
 std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
     char b[256];
-    if (p.persist)
+    if (p.tc)
+        snprintf(b, sizeof b, "tc k_nmf_tc<K=%d> cluster=%d grid=%d ring=%d+%dx%d-bin bins/CTA=%d..%d +k_dred", g.K,
+                 TC_CLUSTER, TC_CLUSTER * p.tc_ncl, p.tc_R, p.tc_R2, p.tc_rg.W, p.tc_rg.L[TC_CLUSTER - 1],
+                 p.tc_rg.L[0]);
+    else if (p.persist)
         snprintf(b, sizeof b, "persist k_nmf_persist<K=%d,LP=%d,NBG=%d,NGRP=%d> grid=%d", g.K, p.LP, p.nbuf,
                  p.ngrp, p.nblk_f);
     else if (p.fused)

@@ -364,8 +364,9 @@ class Hsnct:
         return float(ms[0]), float(ms[1])
 
     def debug_trace(self):
-        """Per-iteration, per-CTA phase stamps of the last persistent decompose (ns), as a
-        uint64 array [iters, n_cta, 8], or None when tracing is off (HSNCT_TRACE=1 at create)."""
+        """%globaltimer stamps (ns) of the last decompose, uint64 [256, n_cta, 16]: per
+        iteration (persistent kernel) or per tile of the last iteration (tcgen05 pass, its
+        first 256 tiles); None when tracing is off (HSNCT_TRACE=1 at create)."""
         import numpy as np
         L = lib()
         n_out, n_cta = ctypes.c_size_t(0), ctypes.c_int(0)
@@ -374,7 +375,7 @@ class Hsnct:
             return None
         buf = np.zeros(n_out.value, dtype=np.uint64)
         _check(L.hsnct_debug_trace(self._h, ctypes.c_void_p(buf.ctypes.data), buf.size, None, None))
-        return buf.reshape(-1, n_cta.value, 8)
+        return buf.reshape(-1, n_cta.value, 16)
 
     def sync(self, stream=None):
         """Wait for the stream; raise the deferred data/numeric status (hsnct_sync)."""

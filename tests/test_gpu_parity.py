@@ -361,7 +361,7 @@ def test_fhr_host_matches_device_path(H):
 def test_fhr_stream_windows_match_device_path(H, wsl):
     """hsnct_fhr_stream: every x^h window is delivered once, in order, and equals the device
     path bit for bit (same kernels on the same inputs); ragged last window (5 slices)."""
-    cfg = sd.custom(idx=41, Nc=24, Nv=12, Nr=5, Nk=70, K=3, M=3)
+    cfg = sd.custom(idx=41, Nc=24, Nv=12, Nr=5, Nk=72, K=3, M=3)
     pr = sd.make_problem(cfg)
     h = H(cfg)
     n = 15
