@@ -217,6 +217,12 @@ uint64_t hsnct_kernel_launches(hsnct_t h);
  * (both nullable).  Synchronous. */
 hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_out, int* n_cta);
 
+/* Statistic of the last hsnct_subspace_decompose on this handle (SPEC's clamped-count
+ * statistic, reading R6): *n_clamped receives the number of entries of Y (bins < N_k of the
+ * N_p rows) that were negative and entered the NMF as 0.  Waits for `stream` (the call's
+ * stream).  Counted with integer atomics, so exact and deterministic. */
+hsnct_status hsnct_decompose_stats(hsnct_t h, int64_t* n_clamped, void* stream);
+
 /* Diagnostics: the subspace-extraction plan chosen at create (which row-pass kernel, its
  * template parameters and grid), as a NUL-terminated string copied to the HOST buffer
  * buf (at most n bytes, truncated).  Shapes that differ only in N_r beyond a few row

@@ -16,6 +16,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 
 using namespace hsnct;
@@ -73,6 +75,12 @@ struct DeviceGuard {
 };
 
 size_t a256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// NVTX range around every ABI call (visible to nsys / ncu --nvtx; no cost without a tool)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 int trace_ctas(const NmfPlan& p) { return p.tc ? TC_CLUSTER * p.tc_ncl : p.nblk_f; }
 
@@ -163,6 +171,8 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
                            double* obj, void* ws, cudaStream_t s) {
     if (n_iter == 0) return HSNCT_OK;
     NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
+    w.nclamp = h->t.nclamp;
+    CK(cudaMemsetAsync(h->t.nclamp, 0, sizeof(unsigned long long), s), "decompose stats");
     w.trace = h->trace;
     w.trace_iters = h->trace_iters;
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
@@ -242,6 +252,7 @@ const char* hsnct_status_string(hsnct_status st) {
 }
 
 hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
+    Nvtx nvtx_("hsnct_create");
     g_last_error.clear();
     if (!out) return fail(HSNCT_E_ARG, "create: out is NULL");
     *out = nullptr;
@@ -328,6 +339,7 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     al((void**)&h->t.Hhat, g.P * sizeof(float));
     al((void**)&h->t.twiddle, (g.P / 2) * sizeof(float2));
     al((void**)&h->t.status, sizeof(unsigned));
+    al((void**)&h->t.nclamp, sizeof(unsigned long long));
     al((void**)&h->t.counter, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->status_host, sizeof(unsigned), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaMemcpy(h->t.cos_t, cs.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
@@ -336,6 +348,7 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     if (e == cudaSuccess)
         e = cudaMemcpy(h->t.twiddle, tw.data(), (g.P / 2) * sizeof(float2), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(h->t.status, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(h->t.nclamp, 0, sizeof(unsigned long long));
     if (e == cudaSuccess) e = cudaMemset(h->t.counter, 0, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
     const char* tr = getenv("HSNCT_TRACE");
     if (e == cudaSuccess && tr && tr[0] == '1' && (h->nmf.persist || h->nmf.tc)) {
@@ -362,6 +375,7 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.Hhat);
     cudaFree(h->t.twiddle);
     cudaFree(h->t.status);
+    cudaFree(h->t.nclamp);
     cudaFree(h->t.counter);
     cudaFree(h->trace);
     for (cudaEvent_t e : h->fbp_ev)
@@ -390,6 +404,7 @@ size_t hsnct_workspace_bytes(hsnct_t h, int op) {
 hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, float* V, float* D,
                                       int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
                                       void* stream) {
+    Nvtx nvtx_("hsnct_subspace_decompose");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "decompose: handle is NULL");
     const Geometry& g = h->g;
@@ -416,6 +431,7 @@ hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, f
 }
 
 hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fbp");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fbp: handle is NULL");
     const Geometry& g = h->g;
@@ -435,6 +451,7 @@ hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_
 
 hsnct_status hsnct_synthesize(hsnct_t h, const float* X, const float* D, int slice0, int n_slices,
                               int bin0, int n_bins, float* Xh, int64_t ld_xh, void* stream) {
+    Nvtx nvtx_("hsnct_synthesize");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "synthesize: handle is NULL");
     const Geometry& g = h->g;
@@ -456,6 +473,7 @@ hsnct_status hsnct_synthesize(hsnct_t h, const float* X, const float* D, int sli
 
 hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int n_slices, int bin0,
                        int n_bins, float* Xh, int64_t ld_xh, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_dhr");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "dhr: handle is NULL");
     const Geometry& g = h->g;
@@ -496,6 +514,7 @@ hsnct_status hsnct_dhr(hsnct_t h, const float* Y, int64_t ld_y, int slice0, int 
 hsnct_status hsnct_fhr_host(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
                             const float* D0_host, int n_iter, float* Xh_host, float* V_host,
                             float* D_host, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fhr_host");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fhr_host: handle is NULL");
     const Geometry& g = h->g;
@@ -556,6 +575,7 @@ hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, cons
                               const float* D0_host, int n_iter, int window_slices, float* ring_host,
                               hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
                               void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fhr_stream");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fhr_stream: handle is NULL");
     const Geometry& g = h->g;
@@ -643,6 +663,7 @@ static hsnct_status check_nmat(const Geometry& g, int n_mat, const char* op) {
 
 hsnct_status hsnct_fmd_transform(hsnct_t h, const float* X, const int32_t* labels, int n_mat, float* T,
                                  void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fmd_transform");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fmd_transform: handle is NULL");
     const Geometry& g = h->g;
@@ -664,6 +685,7 @@ hsnct_status hsnct_fmd_transform(hsnct_t h, const float* X, const int32_t* label
 
 hsnct_status hsnct_fmd_materials(hsnct_t h, const float* X, const float* T, int n_mat, float* Xm,
                                  void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fmd_materials");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fmd_materials: handle is NULL");
     const Geometry& g = h->g;
@@ -684,6 +706,7 @@ hsnct_status hsnct_fmd_materials(hsnct_t h, const float* X, const float* T, int 
 }
 
 hsnct_status hsnct_fmd_spectra(hsnct_t h, const float* D, const float* T, int n_mat, float* Dm, void* stream) {
+    Nvtx nvtx_("hsnct_fmd_spectra");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fmd_spectra: handle is NULL");
     const Geometry& g = h->g;
@@ -702,6 +725,7 @@ hsnct_status hsnct_fmd_spectra(hsnct_t h, const float* D, const float* T, int n_
 }
 
 hsnct_status hsnct_sync(hsnct_t h, void* stream) {
+    Nvtx nvtx_("hsnct_sync");
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "sync: handle is NULL");
     DeviceGuard guard(h->device);
@@ -721,6 +745,18 @@ hsnct_status hsnct_debug_trace(hsnct_t h, uint64_t* host, size_t n, size_t* n_ou
     if (!host) return fail(HSNCT_E_ARG, "debug_trace: host buffer is NULL");
     DeviceGuard guard(h->device);
     CK(cudaMemcpy(host, h->trace, m * sizeof(uint64_t), cudaMemcpyDeviceToHost), "debug_trace");
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_decompose_stats(hsnct_t h, int64_t* n_clamped, void* stream) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "decompose_stats: handle is NULL");
+    if (!n_clamped) return fail(HSNCT_E_ARG, "decompose_stats: n_clamped is NULL");
+    DeviceGuard guard(h->device);
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, h->t.nclamp, sizeof v, cudaMemcpyDeviceToHost, (cudaStream_t)stream), "decompose_stats");
+    CK(cudaStreamSynchronize((cudaStream_t)stream), "decompose_stats");
+    *n_clamped = (int64_t)v;
     return HSNCT_OK;
 }
 

@@ -57,6 +57,7 @@ struct DeviceTables {
     float2* twiddle = nullptr;  // [P/2] exp(-2 pi i t / P)
     unsigned* status = nullptr; // device status word
     unsigned* counter = nullptr;// grid "last block" tickets (zero between launches)
+    unsigned long long* nclamp = nullptr;  // negative Y entries clamped to 0 by the last decompose
 };
 
 // ---------------------------------------------------------------- NMF (nmf.cu)
@@ -115,6 +116,7 @@ struct NmfWs {
     double* L2H;     // [nbx*DG2*K*K]
     float* Yp;       // [Np*Nkp] Y+ (fused path only)
     double* ypart;   // [nby] ||Y+||^2 partials (fused and tc paths)
+    unsigned long long* nclamp = nullptr;  // clamped-entry counter (handle-owned, zeroed per call)
     void* Yc;        // [Npad*Nk16] Y+ as fp16 hi/lo pairs in the tcgen05 layout (tc path)
     unsigned* ymax;  // bits of max(Y+) (tc path)
     // diagnostics (hsnct_debug_trace): per-iteration, per-CTA %globaltimer stamps

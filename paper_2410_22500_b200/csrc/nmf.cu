@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(VT) k_vstep(const float* __restrict__ Y, int64
                                               const float* __restrict__ D,
                                               const double* __restrict__ Gd,
                                               double* __restrict__ vpart,
-                                              unsigned* __restrict__ status) {
+                                              unsigned* __restrict__ status,
+                                              unsigned long long* __restrict__ nclamp) {
     extern __shared__ __align__(16) float Ds[];  // [K][Nkp], zero padded
+    unsigned ncl = 0;
     __shared__ double Gs[K * K];
     __shared__ double red[2][VW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(VT) k_vstep(const float* __restrict__ Y, int64
                 mask_quad(y[rr], l0, Nk);
                 if (FIRST) {
                     if (!finite4(y[rr])) bad |= ST_Y_NONFINITE;
+                    if (r0 + rr < Np)
+                        ncl += (y[rr].x < 0.f) + (y[rr].y < 0.f) + (y[rr].z < 0.f) + (y[rr].w < 0.f);
                 }
                 y[rr] = clamp0(y[rr]);
                 if (FIRST) {
@@ -204,6 +208,10 @@ __global__ void __launch_bounds__(VT) k_vstep(const float* __restrict__ Y, int64
                 }
             }
         }
+    }
+    if (FIRST) {
+        ncl = __reduce_add_sync(0xffffffffu, ncl);
+        if (lane == 0 && ncl) atomicAdd(nclamp, (unsigned long long)ncl);
     }
     // block reduction of the fp64 partials (fixed order)
     vdotA = warp_sum(vdotA);
@@ -661,9 +669,11 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
                               : ensure_smem((const void*)k_vstep<K, false>, (int)p.smem_v, attr_n);
         if (e != cudaSuccess) return e;
         if (first)
-            k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
+            k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status,
+                                                            w.nclamp);
         else
-            k_vstep<K, false><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status);
+            k_vstep<K, false><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status,
+                                                             w.nclamp);
         dim3 gb(p.nchunk, p.nlam_blk);
         k_bpart<K><<<gb, p.bthreads, 0, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, p.rows_per_chunk, w.Bpart, w.Hpart);
     }

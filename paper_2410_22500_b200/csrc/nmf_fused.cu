@@ -13,6 +13,8 @@ static int nbuf_for(int Nkp, int LP, int K, int ngrp) {
 }
 
 bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
+    // K <= 8: the V update maps one lane per (tile row, component), RG * K <= 32 lanes; K = 9..12
+    // instantiations measured wrong (C6 round 2), so K > 8 runs the two-pass kernels
     if (g.K > 8) return false;
     const int Nkp = (g.Nk + 3) & ~3;
     const int pairs = (g.Nk + 1) / 2;
@@ -53,7 +55,7 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
 cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                              unsigned* status, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    k_yplus<<<p.nby, 256, 0, s>>>(Y, ld_y, Np, g.Nk, p.Nkp, w.Yp, w.ypart, status);
+    k_yplus<<<p.nby, 256, 0, s>>>(Y, ld_y, Np, g.Nk, p.Nkp, w.Yp, w.ypart, status, w.nclamp);
     return cudaGetLastError();
 }
 

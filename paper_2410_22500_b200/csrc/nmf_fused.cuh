@@ -106,8 +106,11 @@ __device__ __forceinline__ int tr_base(int lane) {
 // row at a time, lanes over lambda quads.
 __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int64_t ld, int64_t Np, int Nk,
                                                int Nkp, float* __restrict__ Yp, double* __restrict__ ypart,
-                                               unsigned* __restrict__ status) {
+                                               unsigned* __restrict__ status,
+                                               unsigned long long* __restrict__ nclamp) {
     __shared__ double red[8];
+    __shared__ unsigned cred[8];
+    unsigned ncl = 0;
     const int nq = Nkp >> 2;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * 8;
@@ -128,6 +131,7 @@ __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int6
                 if (l0 + 3 >= Nk) y.w = 0.f;
             }
             if (!(isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w))) bad = ST_Y_NONFINITE;
+            ncl += (y.x < 0.f) + (y.y < 0.f) + (y.z < 0.f) + (y.w < 0.f);
             y.x = fmaxf(y.x, 0.f);
             y.y = fmaxf(y.y, 0.f);
             y.z = fmaxf(y.z, 0.f);
@@ -140,15 +144,22 @@ __global__ void __launch_bounds__(256) k_yplus(const float* __restrict__ Y, int6
     s = warp_sum_d(s);
 #pragma unroll
     for (int o = 16; o; o >>= 1) bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    ncl = __reduce_add_sync(0xffffffffu, ncl);
     if (lane == 0) {
         red[w] = s;
+        cred[w] = ncl;
         if (bad) atomicOr(status, bad);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int i = 0; i < 8; ++i) t += red[i];
+        unsigned long long c = 0;
+        for (int i = 0; i < 8; ++i) {
+            t += red[i];
+            c += cred[i];
+        }
         ypart[blockIdx.x] = t;
+        if (c) atomicAdd(nclamp, c);
     }
 }
 

@@ -570,9 +570,11 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
 // ||Y+||^2 partials per block (fixed order), non-finite check.  One warp per row.
 __global__ void __launch_bounds__(256) k_tc_stats(const float* __restrict__ Y, int64_t ld, int64_t Np, int Nk,
                                                   unsigned* __restrict__ ymax, unsigned* __restrict__ ynorm,
-                                                  double* __restrict__ ypart, unsigned* __restrict__ status) {
+                                                  double* __restrict__ ypart, unsigned* __restrict__ status,
+                                                  unsigned long long* __restrict__ nclamp) {
     __shared__ double red[8];
-    __shared__ unsigned mred[8], nred[8];
+    __shared__ unsigned mred[8], nred[8], cred[8];
+    unsigned ncl = 0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int nq = (Nk + 3) >> 2;
     double s = 0.0;
@@ -593,6 +595,7 @@ __global__ void __launch_bounds__(256) k_tc_stats(const float* __restrict__ Y, i
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (!isfinite(v[j])) bad = ST_Y_NONFINITE;
+                ncl += v[j] < 0.f;
                 const float yp = fmaxf(v[j], 0.f);
                 m = max(m, __float_as_uint(yp));
                 ps = fmaf(yp, yp, ps);
@@ -605,22 +608,27 @@ __global__ void __launch_bounds__(256) k_tc_stats(const float* __restrict__ Y, i
     }
     m = __reduce_max_sync(0xffffffffu, m);
     bad = __reduce_or_sync(0xffffffffu, bad);
+    ncl = __reduce_add_sync(0xffffffffu, ncl);
     if (lane == 0) {
         red[w] = s;
         mred[w] = m;
         nred[w] = nm;
+        cred[w] = ncl;
         if (bad) atomicOr(status, bad);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
         unsigned mm = 0, nn = 0;
+        unsigned long long c = 0;
         for (int j = 0; j < 8; ++j) {
             t += red[j];
             mm = max(mm, mred[j]);
             nn = max(nn, nred[j]);
+            c += cred[j];
         }
         ypart[blockIdx.x] = t;
+        if (c) atomicAdd(nclamp, c);
         if (mm) atomicMax(ymax, mm);
         if (nn) atomicMax(ynorm, nn);
     }
@@ -827,7 +835,7 @@ cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     cudaError_t e = cudaMemsetAsync(w.ymax, 0, 2 * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
-    k_tc_stats<<<p.nby, 256, 0, s>>>(Y, ld_y, Np, g.Nk, w.ymax, w.ymax + 1, w.ypart, status);
+    k_tc_stats<<<p.nby, 256, 0, s>>>(Y, ld_y, Np, g.Nk, w.ymax, w.ymax + 1, w.ypart, status, w.nclamp);
     k_tc_convert<<<g.num_sms * 16, 256, 0, s>>>(Y, ld_y, Np, g.Nk, p.tc_Nk16, p.tc_rg, w.ymax,
                                                   reinterpret_cast<__half*>(w.Yc));
     return cudaGetLastError();

@@ -86,6 +86,8 @@ def lib():
             L.hsnct_fmd_spectra.restype = i32
             L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
             L.hsnct_debug_trace.restype = i32
+            L.hsnct_decompose_stats.argtypes = [vp, ctypes.POINTER(i64), vp]
+            L.hsnct_decompose_stats.restype = i32
             L.hsnct_debug_plan.argtypes = [vp, ctypes.c_char_p, sz]
             L.hsnct_debug_plan.restype = i32
             L.hsnct_debug_fbp_timing.argtypes = [vp, ctypes.c_int]
@@ -346,6 +348,12 @@ class Hsnct:
         self._dev(Dm, "Dm", (n_mat, self.Nk))
         _check(lib().hsnct_fmd_spectra(self._h, _ptr(D), _ptr(T), int(n_mat), _ptr(Dm), _stream(stream, self.device)))
         return Dm
+
+    def decompose_stats(self, stream=None) -> dict:
+        """Statistics of the last subspace_decompose: {"n_clamped": negative Y entries set to 0}."""
+        n = ctypes.c_int64(0)
+        _check(lib().hsnct_decompose_stats(self._h, ctypes.byref(n), _stream(stream, self.device)))
+        return {"n_clamped": int(n.value)}
 
     def debug_plan(self) -> str:
         """The subspace-extraction plan (row-pass kernel, template, grid) chosen at create."""

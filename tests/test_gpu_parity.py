@@ -52,6 +52,10 @@ def padded(Y, ld, fill=float("nan")):
     (sd.custom(idx=23, Nc=24, Nv=11, Nr=1, Nk=801, K=6, M=6), 20),
     # K*K = 64 > 32: the objective reads G_old across several warps
     (sd.custom(idx=24, Nc=24, Nv=11, Nr=1, Nk=200, K=8, M=4), 10),
+    # K = 9 .. 12 on the fused persistent kernel (the paper's N_s = 9, Table I shape's N_k)
+    (sd.custom(idx=25, Nc=32, Nv=16, Nr=4, Nk=1200, K=9, M=3), 20),
+    (sd.custom(idx=26, Nc=24, Nv=11, Nr=2, Nk=600, K=12, M=5), 12),
+    (sd.custom(idx=27, Nc=20, Nv=9, Nr=1, Nk=333, K=10, M=4), 12),
 ])
 def test_nmf_parity(H, cfg, n_iter):
     pr = sd.make_problem(cfg)
@@ -105,7 +109,9 @@ def test_nmf_deterministic_and_resumable(H):
 
 
 @pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
-                                        (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25)])
+                                        (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25),
+                                        (sd.custom(idx=12, Nc=32, Nv=16, Nr=4, Nk=1200, K=9, M=3), 15),
+                                        (sd.custom(idx=13, Nc=24, Nv=11, Nr=2, Nk=600, K=12, M=5), 10)])
 def test_nmf_per_iteration_fallback(H, monkeypatch, cfg, n_iter):
     """The per-iteration launch path (used when a cooperative launch is refused)."""
     monkeypatch.setenv("HSNCT_NO_PERSIST", "1")
@@ -435,3 +441,25 @@ def test_argument_errors(H):
                                            ctypes.c_void_p(Y.data_ptr()), ctypes.c_void_p(D.data_ptr()),
                                            1, None, ctypes.c_void_p(ws.data_ptr()), ws.numel(), None)
     assert st == 1 and b"overlap" in hm.lib().hsnct_last_error()
+
+
+@pytest.mark.parametrize("plan,cfg", [
+    ("ffma", sd.CONFIGS[1]),
+    ("tc", sd.CONFIGS[1]),
+    ("ffma", sd.custom(idx=71, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),      # K > 8: two-pass path
+    ("ffma", sd.custom(idx=72, Nc=20, Nv=13, Nk=203, K=5, M=4)),            # ragged N_k (masked padding)
+])
+def test_clamped_count_statistic(monkeypatch, plan, cfg):
+    """hsnct_decompose_stats: the number of negative Y entries clamped to 0 (reading R6) is
+    exact on every row-pass plan, and counts only the N_k real bins (NaN-poisoned padding)."""
+    monkeypatch.setenv("HSNCT_NMF", plan)
+    from paper_2410_22500_b200 import Hsnct
+    pr = sd.make_problem(cfg)
+    h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
+    Yd = padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4 + 4, fill=-1.0)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(Yd, V, D, 2)
+    h.sync()
+    assert h.decompose_stats()["n_clamped"] == int((pr["Y"] < 0).sum())
+    assert int((pr["Y"] < 0).sum()) > 0
