@@ -30,6 +30,20 @@ constexpr int BROWS = 32;      // V rows staged per column-pass sub-chunk
 // C3 / C5 against the persistent FFMA kernel's 0.72 (profiles/r02/tc/)
 constexpr int64_t TC_MIN_ROWS = INT64_MAX;
 
+// two independent fp32 FMAs in one packed instruction (fma.rn.f32x2): same rounding as FFMA
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\t"
+        "mov.b64 rb, {%4, %5};\n\t"
+        "mov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\t"
+        "mov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+
 __device__ __forceinline__ float4 ld4(const float* p) {
     return __ldg(reinterpret_cast<const float4*>(p));
 }
@@ -158,17 +172,20 @@ __global__ void __launch_bounds__(VT) k_vstep(const float* __restrict__ Y, int64
                     ys[rr] = fmaf(y[rr].w, y[rr].w, ys[rr]);
                 }
             }
+            // rows in pairs: one packed FMA per (row pair, component, bin), the same per-row
+            // summation order as scalar FFMA
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 const float4 d = reinterpret_cast<const float4*>(Ds + k * Nkp)[q];
 #pragma unroll
-                for (int rr = 0; rr < RPW; ++rr) {
-                    float a = acc[rr][k];
-                    a = fmaf(y[rr].x, d.x, a);
-                    a = fmaf(y[rr].y, d.y, a);
-                    a = fmaf(y[rr].z, d.z, a);
-                    a = fmaf(y[rr].w, d.w, a);
-                    acc[rr][k] = a;
+                for (int rr = 0; rr < RPW; rr += 2) {
+                    float2 a = make_float2(acc[rr][k], acc[rr + 1][k]);
+                    a = fma2(make_float2(y[rr].x, y[rr + 1].x), make_float2(d.x, d.x), a);
+                    a = fma2(make_float2(y[rr].y, y[rr + 1].y), make_float2(d.y, d.y), a);
+                    a = fma2(make_float2(y[rr].z, y[rr + 1].z), make_float2(d.z, d.z), a);
+                    a = fma2(make_float2(y[rr].w, y[rr + 1].w), make_float2(d.w, d.w), a);
+                    acc[rr][k] = a.x;
+                    acc[rr + 1][k] = a.y;
                 }
             }
         }
@@ -250,9 +267,9 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
     const int64_t re = min(Np, rb0 + rpc);
     constexpr int HPT = (K * K + 31) / 32;  // H outputs per thread (blockDim >= 32)
     const bool do_h = blockIdx.y == 0;
-    float4 acc[K];
+    float2 axy[K], azw[K];  // B partial of the quad: bins (l0, l0+1) and (l0+2, l0+3), packed FMAs
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < K; ++k) axy[k] = azw[k] = make_float2(0.f, 0.f);
     double h[HPT];
 #pragma unroll
     for (int j = 0; j < HPT; ++j) h[j] = 0.0;
@@ -277,10 +294,8 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
                         const float v = Vs[(i + u) * K + k];
-                        acc[k].x = fmaf(v, y[u].x, acc[k].x);
-                        acc[k].y = fmaf(v, y[u].y, acc[k].y);
-                        acc[k].z = fmaf(v, y[u].z, acc[k].z);
-                        acc[k].w = fmaf(v, y[u].w, acc[k].w);
+                        axy[k] = fma2(make_float2(v, v), make_float2(y[u].x, y[u].y), axy[k]);
+                        azw[k] = fma2(make_float2(v, v), make_float2(y[u].z, y[u].w), azw[k]);
                     }
                 }
             }
@@ -291,10 +306,8 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const float v = Vs[i * K + k];
-                    acc[k].x = fmaf(v, y.x, acc[k].x);
-                    acc[k].y = fmaf(v, y.y, acc[k].y);
-                    acc[k].z = fmaf(v, y.z, acc[k].z);
-                    acc[k].w = fmaf(v, y.w, acc[k].w);
+                    axy[k] = fma2(make_float2(v, v), make_float2(y.x, y.y), axy[k]);
+                    azw[k] = fma2(make_float2(v, v), make_float2(y.z, y.w), azw[k]);
                 }
             }
         }
@@ -314,7 +327,8 @@ __global__ void __launch_bounds__(BT_MAX) k_bpart(const float* __restrict__ Y, i
     if (qv) {
 #pragma unroll
         for (int k = 0; k < K; ++k)
-            reinterpret_cast<float4*>(Bpart + ((int64_t)blockIdx.x * K + k) * Nkp)[q] = acc[k];
+            reinterpret_cast<float4*>(Bpart + ((int64_t)blockIdx.x * K + k) * Nkp)[q] =
+                make_float4(axy[k].x, axy[k].y, azw[k].x, azw[k].y);
     }
     if (do_h) {
 #pragma unroll
@@ -560,7 +574,9 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.nlam_blk = (nq + BT_MAX - 1) / BT_MAX;
     const int per = (nq + p.nlam_blk - 1) / p.nlam_blk;
     p.bthreads = std::max(32, ((per + 31) / 32) * 32);
-    const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 2) / p.nlam_blk);
+    // row chunks of the column pass: ~8 blocks of up to 128 threads per SM in flight (it streams
+    // Y from HBM with a long dependent loop per thread; 2 per SM measured 12% warps active)
+    const int64_t want = std::max<int64_t>(1, ((int64_t)num_sms * 8) / p.nlam_blk);
     p.nchunk = (int)std::max<int64_t>(1, std::min<int64_t>(want, (Np + BROWS - 1) / BROWS));
     p.rows_per_chunk = (Np + p.nchunk - 1) / p.nchunk;
     p.nchunk = (int)((Np + p.rows_per_chunk - 1) / p.rows_per_chunk);
