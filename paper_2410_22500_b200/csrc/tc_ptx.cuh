@@ -121,6 +121,27 @@ __device__ __forceinline__ void mma_f16_warp(uint32_t tmem_d, uint64_t adesc, ui
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// The same with the A operand in TMEM (lane m = row m of A, 2 fp16 of K per column; K = 16 ->
+// 8 columns at tmem_a), B from shared memory.
+__device__ __forceinline__ void mma_f16_tmem_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                  uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// shared memory -> TMEM: 128 rows x 256 bits of a K-major no-swizzle matrix; row r lands in
+// lane r, 8 columns (measured: profiles/r02/microbench/tc05_tmemA.txt).  Asynchronous; ordered
+// with the issuing thread's later tcgen05 operations, completion tracked by tcgen05.commit.
+__device__ __forceinline__ void tmem_cp_128x256b_warp(uint32_t tmem_dst, uint64_t sdesc_src) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(tmem_dst),
+        "l"(sdesc_src)
+        : "memory");
+}
 // commit by the elected lane of a converged warp (the lane that issued the warp's MMAs)
 __device__ __forceinline__ void mma_commit_warp(uint64_t* b) {
     asm volatile(
