@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dhr", action="store_true")
     ap.add_argument("--no-fmd", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="N > 1: split the config's slices over the ranks (strong scaling; one NCCL "
+                         "all-reduce of B, H and two scalars per NMF iteration, NEXT-4) instead of replicas")
     return ap.parse_args()
 
 
@@ -142,11 +145,13 @@ def workload_desc(cfg, n_iter):
             f"Poisson {cfg.counts:g} counts/bin")
 
 
-def config_dict(cfg, n_iter, world):
+def config_dict(cfg, n_iter, world, shard=False):
     """The `config` object of BOTH arms' JSON lines (identical by construction)."""
+    par = (f"slice-sharded x{world} (one all-reduce of B, H, 2 scalars per NMF iteration)" if shard
+           else f"replicas x{world}")
     return {"workload": workload_desc(cfg, n_iter), "config_index": cfg.idx,
             "Nc": cfg.Nc, "Nr": cfg.Nr, "Nv": cfg.Nv, "Nk": cfg.Nk, "K": cfg.K,
-            "n_iter": n_iter, "parallelism": f"replicas x{world}",
+            "n_iter": n_iter, "parallelism": par,
             "l2": f"inputs larger than L2 (Y = {4 * cfg.Np * cfg.Nk / 1e6:.0f} MB > 126 MB), no flush"}
 
 
@@ -235,7 +240,7 @@ def run_reference(args, cfg, n_iter, rank, world):
             "ms_per_step": T_sample * 1e3, "full_step_ms_extrapolated": T_full * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Bragg-edge ellipse phantom, Poisson counts, -log)",
-            "config": config_dict(cfg, n_iter, world),
+            "config": config_dict(cfg, n_iter, world, args.shard),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": smp["threads"], "kind": "oracle",
                              "sample": smp["desc"], "extrapolated": smp["extrapolated"],
                              "sample_fraction_of_step": smp["fraction"], "wall_s": wall},
@@ -260,6 +265,20 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
 
     pr = sd.make_problem(cfg, device=dev)
     Y, V0, D0 = pr["Y"], pr["V0"], pr["D0"]
+    shard = args.shard  # at N = 1 the split iteration without a collective (a path check)
+    gcfg = cfg  # the global workload (the metric counts its voxel*lambda)
+    if shard:
+        # this rank's slices [r0, r1): all views of them, local row order (v, r - r0, c); the
+        # extras below (DHR, FMD, e2e, CPU baseline) are single-GPU measurements and skipped
+        from paper_2410_22500_b200.sharded import slice_range, slice_rows
+        r0, r1 = slice_range(cfg.Nr, rank, world)
+        if world > 1:
+            rows = slice_rows(cfg.Nv, cfg.Nr, cfg.Nc, r0, r1).to(dev)
+            Y, V0 = Y.index_select(0, rows), V0.index_select(0, rows)
+            pr["Y"], pr["V0"] = Y, V0
+            torch.cuda.empty_cache()
+        cfg = sd.reduced(cfg, r1 - r0)
+        args.no_dhr = args.no_fmd = args.no_e2e = args.no_cpu = True
     h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=local_rank)
     V = torch.empty_like(V0)
     D = torch.empty_like(D0)
@@ -273,12 +292,18 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    red = torch.empty(h.nmf_red_size(), dtype=torch.float64, device=dev) if shard else None
+
     def step(rec=None):
         V.copy_(V0)
         D.copy_(D0)
         if rec is not None:
             rec[0].record(stream)
-        h.subspace_decompose(Y, V, D, n_iter, ws=ws_nmf)
+        if shard:
+            from paper_2410_22500_b200.sharded import sharded_subspace_decompose
+            sharded_subspace_decompose(h, Y, V, D, n_iter, ws=ws_nmf, red=red)
+        else:
+            h.subspace_decompose(Y, V, D, n_iter, ws=ws_nmf)
         if rec is not None:
             rec[1].record(stream)
         h.fbp(V, X, ws=ws_fbp)
@@ -315,7 +340,8 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     t_nmf = statistics.mean(r[0].elapsed_time(r[1]) for r in recs) * 1e-3
     t_fbp = statistics.mean(r[1].elapsed_time(r[2]) for r in recs) * 1e-3
     t_syn = statistics.mean(r[2].elapsed_time(r[3]) for r in recs) * 1e-3
-    value = cfg.Nx * cfg.Nk * world / (ms_step * 1e-3)
+    # replicas: every rank does the whole workload; sharded: the ranks share one workload
+    value = gcfg.Nx * gcfg.Nk * (1 if shard else world) / (ms_step * 1e-3)
 
     # rooflines (algorithmic bytes)
     Np, Nk, K, Nx = cfg.Np, cfg.Nk, cfg.K, cfg.Nx
@@ -483,9 +509,9 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "scaling": "strong" if shard else "weak", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic (seeded Bragg-edge ellipse phantom, Poisson counts, -log)",
-                "config": config_dict(cfg, n_iter, world),
+                "config": config_dict(gcfg, n_iter, world, shard),
                 "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

@@ -128,6 +128,33 @@ hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, f
                                       int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
                                       void* stream);
 
+/* Sharded subspace extraction (NEXT-4): Eq. 4 on Y distributed over ranks by
+ * rows (e.g. slice ranges: parallel-beam slices decouple, so a rank's rows are all views of its
+ * slices).  The iteration of hsnct_subspace_decompose, split at its one exchange step:
+ *
+ *   hsnct_nmf_begin(Y, D)                     once: Y+ preparation, G = D D^T
+ *   for it in 0..n_iter-1:
+ *     hsnct_nmf_rowpass(Y, V, D, it, red)     this rank's rows: V half-step (row-local) and its
+ *                                             sums red = [B = V^T Y+ (K x N_k) | H = V^T V (K x K)
+ *                                             | <V_new, A> | ||Y+||^2], fp64
+ *     (caller) all-reduce SUM of red over the ranks, e.g. NCCL via torch.distributed
+ *     hsnct_nmf_dupdate(D, red, it, obj2)     D <- D .* B ./ max(H D, 1e-30) from the global
+ *                                             sums, G for the next row pass, the two objective
+ *                                             values (obj2, device fp64[2], nullable)
+ *
+ * Every rank holds the full D (K x N_k, identical on all ranks) and its own rows of Y and V;
+ * the handle is created with the rank's local geometry (its N_r slices).  On one rank the
+ * sequence computes what hsnct_subspace_decompose computes (up to the order of the fp64 sums).
+ * ws: HSNCT_OP_DECOMPOSE workspace of the handle, reused across the calls of one decomposition.
+ * red: device fp64 array of hsnct_nmf_red_size(h) values.  Errors as hsnct_subspace_decompose. */
+size_t hsnct_nmf_red_size(hsnct_t h);
+hsnct_status hsnct_nmf_begin(hsnct_t h, const float* Y, int64_t ld_y, const float* D, void* ws, size_t ws_bytes,
+                             void* stream);
+hsnct_status hsnct_nmf_rowpass(hsnct_t h, const float* Y, int64_t ld_y, float* V, const float* D, int it, void* ws,
+                               size_t ws_bytes, double* red, void* stream);
+hsnct_status hsnct_nmf_dupdate(hsnct_t h, float* D, const double* red, int it, double* obj2, void* ws,
+                               size_t ws_bytes, void* stream);
+
 /* FBP of the K subspace sinograms (Algorithm 1 lines "Tomographic
  * Reconstruction", FBP per R10): column k of V, reshaped
  * (N_v, N_r, N_c), is ramp-filtered along c and backprojected into X[k].

@@ -430,6 +430,77 @@ hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, f
     return run_decompose(h, Y, ld_y, V, D, n_iter, obj_trace, ws, (cudaStream_t)stream);
 }
 
+size_t hsnct_nmf_red_size(hsnct_t h) { return h ? nmf_red_size(h->g) : 0; }
+
+hsnct_status hsnct_nmf_begin(hsnct_t h, const float* Y, int64_t ld_y, const float* D, void* ws, size_t ws_bytes,
+                             void* stream) {
+    Nvtx nvtx_("hsnct_nmf_begin");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "nmf_begin: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_y(g, Y, ld_y, "nmf_begin");
+    if (st) return st;
+    if (!D || !aligned(D, 4)) return fail(HSNCT_E_ARG, "nmf_begin: D is NULL or misaligned");
+    const size_t need = a256(nmf_ws_bytes(g, h->nmf));
+    if ((st = check_ws(ws, ws_bytes, need, "nmf_begin"))) return st;
+    DeviceGuard guard(h->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    NmfWs w = nmf_ws_carve(g, h->nmf, ws);
+    w.nclamp = h->t.nclamp;
+    CK(cudaMemsetAsync(h->t.nclamp, 0, sizeof(unsigned long long), s), "nmf_begin");
+    CK(nmf_launch_init(g, h->nmf, w, Y, ld_y, D, h->t.status, s), "nmf_begin");
+    h->launches += nmf_init_launches(h->nmf);
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_nmf_rowpass(hsnct_t h, const float* Y, int64_t ld_y, float* V, const float* D, int it, void* ws,
+                               size_t ws_bytes, double* red, void* stream) {
+    Nvtx nvtx_("hsnct_nmf_rowpass");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "nmf_rowpass: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_y(g, Y, ld_y, "nmf_rowpass");
+    if (st) return st;
+    if (!V || !D || !red) return fail(HSNCT_E_ARG, "nmf_rowpass: V, D or red is NULL");
+    if (!aligned(V, 16) || !aligned(D, 4) || !aligned(red, 8))
+        return fail(HSNCT_E_ARG, "nmf_rowpass: V must be 16-byte, D 4-byte and red 8-byte aligned");
+    if (it < 0) return fail(HSNCT_E_ARG, "nmf_rowpass: it=%d < 0", it);
+    const size_t need = a256(nmf_ws_bytes(g, h->nmf));
+    if ((st = check_ws(ws, ws_bytes, need, "nmf_rowpass"))) return st;
+    const Range rV = rng(V, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rR = rng(red, nmf_red_size(g) * sizeof(double));
+    if (overlap(rV, rR) || overlap(rR, rng(ws, need)) || overlap(rV, rng(ws, need)) ||
+        overlap(rV, rng(D, (size_t)g.K * g.Nk * sizeof(float))))
+        return fail(HSNCT_E_ARG, "nmf_rowpass: V, D, red and the workspace must not overlap");
+    DeviceGuard guard(h->device);
+    NmfWs w = nmf_ws_carve(g, h->nmf, ws);
+    w.nclamp = h->t.nclamp;
+    CK(nmf_shard_rowpass(g, h->nmf, w, Y, ld_y, V, D, it, red, h->t.status, (cudaStream_t)stream), "nmf_rowpass");
+    h->launches += nmf_launches_per_iter(h->nmf);  // row pass (+ column pass) + the local reduction
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_nmf_dupdate(hsnct_t h, float* D, const double* red, int it, double* obj2, void* ws,
+                               size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_nmf_dupdate");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "nmf_dupdate: handle is NULL");
+    const Geometry& g = h->g;
+    if (!D || !red) return fail(HSNCT_E_ARG, "nmf_dupdate: D or red is NULL");
+    if (!aligned(D, 4) || !aligned(red, 8) || (obj2 && !aligned(obj2, 8)))
+        return fail(HSNCT_E_ARG, "nmf_dupdate: D, red or obj2 misaligned");
+    if (it < 0) return fail(HSNCT_E_ARG, "nmf_dupdate: it=%d < 0", it);
+    const size_t need = a256(nmf_ws_bytes(g, h->nmf));
+    hsnct_status st;
+    if ((st = check_ws(ws, ws_bytes, need, "nmf_dupdate"))) return st;
+    DeviceGuard guard(h->device);
+    NmfWs w = nmf_ws_carve(g, h->nmf, ws);
+    CK(nmf_shard_dupdate(g, h->nmf, w, D, red, it, obj2, h->t.status, h->t.counter, (cudaStream_t)stream),
+       "nmf_dupdate");
+    h->launches += 1;
+    return HSNCT_OK;
+}
+
 hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_bytes, void* stream) {
     Nvtx nvtx_("hsnct_fbp");
     g_last_error.clear();

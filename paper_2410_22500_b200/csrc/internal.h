@@ -154,6 +154,13 @@ cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
 cudaError_t nmf_tc_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                           unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
+// sharded decomposition (NEXT-4): one row pass -> the rank's sums in red (fp64 [K*N_k + K*K + 2]);
+// the D update from the all-reduced sums (identical on every rank)
+size_t nmf_red_size(const Geometry& g);
+cudaError_t nmf_shard_rowpass(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                              float* V, const float* D, int it, double* red, unsigned* status, cudaStream_t s);
+cudaError_t nmf_shard_dupdate(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* D, const double* red,
+                              int it, double* obj2, unsigned* status, unsigned* counter, cudaStream_t s);
 std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p);
 // counter words needed by the handle: 1 + ceil(Nk / 32)
 

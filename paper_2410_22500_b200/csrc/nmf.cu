@@ -362,8 +362,10 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 //   last of the DG2 blocks of column bx: B, H in a fixed order, D update for its
 //                   32 lambdas, <B, D_new> and (D_new D_new^T) partials.
 //   last column block overall: G for the next row pass and the objective terms.
-template <int K>
-__global__ void __launch_bounds__(256) k_dred(const float* __restrict__ Bpart,
+// BT: type of the B partials -- float (per-CTA partials of one GPU) or double (the sums of a
+// sharded decomposition, already reduced over CTAs and ranks: P = 1)
+template <int K, typename BT = float>
+__global__ void __launch_bounds__(256) k_dred(const BT* __restrict__ Bpart,
                                               const double* __restrict__ Hpart, int P, int PH, int Nk, int Nkp,
                                               float* __restrict__ D, double* __restrict__ Gd,
                                               const double* __restrict__ vpart, int nblk_v,
@@ -530,6 +532,48 @@ __global__ void __launch_bounds__(256) k_dred(const float* __restrict__ Bpart,
             obj2[1] = sc[0] - 2.0 * sc[2] + hg_new;
         }
         *counter = 0u;
+    }
+}
+
+// ------------------------------------------------------ sharded decomposition (NEXT-4)
+// The per-CTA partials of one row pass reduced in a fixed order into red (fp64):
+//   red[k*Nk + l] = sum_c Bpart[c][k][l],  red[K*Nk + o] = sum_c Hpart[c][o],
+//   red[K*Nk + KK] = sum_c vpart[2c] (<V_new, A>),
+//   red[K*Nk + KK + 1] = sum_c vpart[2c+1] + sum_b ypart[b] (||Y+||^2; used on the first iteration)
+// Grid: ceil(K*Nk / 256) blocks over (k, l); block 0 also reduces H and the scalars.
+template <int K>
+__global__ void __launch_bounds__(256) k_red_local(const float* __restrict__ Bpart, int P, int Nk, int Nkp,
+                                                   const double* __restrict__ Hpart, int PH,
+                                                   const double* __restrict__ vpart, int nvp,
+                                                   const double* __restrict__ ypart, int nby,
+                                                   double* __restrict__ red) {
+    constexpr int KK = K * K;
+    __shared__ double sred[8];
+    const int i = blockIdx.x * 256 + threadIdx.x;
+    if (i < K * Nk) {
+        const int k = i / Nk, l = i - k * Nk;
+        double s = 0.0;
+        for (int c = 0; c < P; ++c) s += (double)__ldcg(Bpart + ((int64_t)c * K + k) * Nkp + l);
+        red[i] = s;
+    }
+    if (blockIdx.x == 0) {
+        for (int o = threadIdx.x; o < KK; o += 256) {
+            double s = 0.0;
+            for (int c = 0; c < PH; ++c) s += __ldcg(Hpart + (int64_t)c * KK + o);
+            red[K * Nk + o] = s;
+        }
+        double v0 = 0.0, v1 = 0.0;
+        for (int c = threadIdx.x; c < nvp; c += 256) {
+            v0 += __ldcg(vpart + 2 * c);
+            v1 += __ldcg(vpart + 2 * c + 1);
+        }
+        for (int b = threadIdx.x; b < nby; b += 256) v1 += __ldcg(ypart + b);
+        const double a = block_sum(v0, sred);
+        const double y = block_sum(v1, sred);
+        if (threadIdx.x == 0) {
+            red[K * Nk + KK] = a;
+            red[K * Nk + KK + 1] = y;
+        }
     }
 }
 
@@ -702,6 +746,78 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
 }
 
 int nmf_launches_per_iter(const NmfPlan& p) { return (p.fused || p.tc) ? 2 : 3; }
+
+// ------------------------------------------------------ sharded decomposition (NEXT-4)
+size_t nmf_red_size(const Geometry& g) { return (size_t)g.K * g.Nk + (size_t)g.K * g.K + 2; }
+
+template <int K>
+static cudaError_t shard_rowpass_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld,
+                                   float* V, const float* D, int it, double* red, unsigned* status, cudaStream_t s) {
+    const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
+    const bool first = it == 0;
+    if (p.tc) {
+        cudaError_t e = nmf_tc_launch(g, p, w, V, D, it, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.fused) {
+        cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
+        if (e != cudaSuccess) return e;
+    } else {
+        static SmemAttr attr_f, attr_n;
+        cudaError_t e = first ? ensure_smem((const void*)k_vstep<K, true>, (int)p.smem_v, attr_f)
+                              : ensure_smem((const void*)k_vstep<K, false>, (int)p.smem_v, attr_n);
+        if (e != cudaSuccess) return e;
+        if (first)
+            k_vstep<K, true><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status,
+                                                            w.nclamp);
+        else
+            k_vstep<K, false><<<p.nblk_v, VT, p.smem_v, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, D, w.Gd, w.vpart, status,
+                                                             w.nclamp);
+        dim3 gb(p.nchunk, p.nlam_blk);
+        k_bpart<K><<<gb, p.bthreads, 0, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, p.rows_per_chunk, w.Bpart, w.Hpart);
+    }
+    const bool yp = p.fused || p.tc;
+    k_red_local<K><<<(K * g.Nk + 255) / 256, 256, 0, s>>>(w.Bpart, p.P, g.Nk, p.Nkp, w.Hpart, p.PH, w.vpart, p.nvp,
+                                                          yp ? w.ypart : nullptr, yp ? p.nby : 0, red);
+    return cudaGetLastError();
+}
+
+template <int K>
+static cudaError_t shard_dupdate_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* D, const double* red,
+                                   int it, double* obj2, unsigned* status, unsigned* counter, cudaStream_t s) {
+    constexpr int KK = K * K;
+    dim3 gd(p.nbx, DG2);
+    // the global sums as one "partial": B [K][N_k] (stride N_k), H, {<V, A>, ||Y+||^2}
+    k_dred<K, double><<<gd, 256, 0, s>>>(red, red + (size_t)K * g.Nk, 1, 1, g.Nk, g.Nk, D, w.Gd,
+                                         red + (size_t)K * g.Nk + KK, 1, nullptr, 0, w.L2B, w.L2H, w.dpart,
+                                         w.Gpart, w.ysq, it == 0 ? 1 : 0, obj2, counter + 1, counter, status);
+    return cudaGetLastError();
+}
+
+cudaError_t nmf_shard_rowpass(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                              float* V, const float* D, int it, double* red, unsigned* status, cudaStream_t s) {
+    switch (g.K) {
+#define M(KV) \
+    case KV:  \
+        return shard_rowpass_k<KV>(g, p, w, Y, ld_y, V, D, it, red, status, s);
+        HSNCT_K_CASES(M)
+#undef M
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t nmf_shard_dupdate(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* D, const double* red,
+                              int it, double* obj2, unsigned* status, unsigned* counter, cudaStream_t s) {
+    switch (g.K) {
+#define M(KV) \
+    case KV:  \
+        return shard_dupdate_k<KV>(g, p, w, D, red, it, obj2, status, counter, s);
+        HSNCT_K_CASES(M)
+#undef M
+        default:
+            return cudaErrorInvalidValue;
+    }
+}
 
 std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
     char b[256];

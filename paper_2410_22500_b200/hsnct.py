@@ -86,6 +86,14 @@ def lib():
             L.hsnct_fmd_spectra.restype = i32
             L.hsnct_debug_trace.argtypes = [vp, vp, sz, ctypes.POINTER(sz), ctypes.POINTER(ctypes.c_int)]
             L.hsnct_debug_trace.restype = i32
+            L.hsnct_nmf_red_size.argtypes = [vp]
+            L.hsnct_nmf_red_size.restype = sz
+            L.hsnct_nmf_begin.argtypes = [vp, vp, i64, vp, vp, sz, vp]
+            L.hsnct_nmf_begin.restype = i32
+            L.hsnct_nmf_rowpass.argtypes = [vp, vp, i64, vp, vp, i32, vp, sz, vp, vp]
+            L.hsnct_nmf_rowpass.restype = i32
+            L.hsnct_nmf_dupdate.argtypes = [vp, vp, vp, i32, vp, vp, sz, vp]
+            L.hsnct_nmf_dupdate.restype = i32
             L.hsnct_decompose_stats.argtypes = [vp, ctypes.POINTER(i64), vp]
             L.hsnct_decompose_stats.restype = i32
             L.hsnct_debug_plan.argtypes = [vp, ctypes.c_char_p, sz]
@@ -200,6 +208,36 @@ class Hsnct:
                                               _ptr(obj_trace), _ptr(ws), ws.numel() * ws.element_size(),
                                               _stream(stream, self.device)))
         return V, D
+
+    # -- sharded decomposition (NEXT-4): the iteration split at its exchange step -------------
+    def nmf_red_size(self) -> int:
+        return int(lib().hsnct_nmf_red_size(self._h))
+
+    def nmf_begin(self, Y, D, ws=None, stream=None):
+        """Y+ preparation and G = D D^T for a sharded decomposition (hsnct_nmf_begin)."""
+        ld = self._rows(Y, "Y", self.Np, self.Nk)
+        self._dev(D, "D", (self.K, self.Nk))
+        ws = self.workspace(OP_DECOMPOSE) if ws is None else ws
+        _check(lib().hsnct_nmf_begin(self._h, _ptr(Y), ld, _ptr(D), _ptr(ws), ws.numel() * ws.element_size(),
+                                     _stream(stream, self.device)))
+
+    def nmf_rowpass(self, Y, V, D, it, red, ws=None, stream=None):
+        """This rank's row pass of iteration `it`; its sums -> red (hsnct_nmf_rowpass)."""
+        ld = self._rows(Y, "Y", self.Np, self.Nk)
+        self._dev(V, "V", (self.Np, self.K))
+        self._dev(D, "D", (self.K, self.Nk))
+        if red.dtype != torch.float64 or red.device != self.device or red.numel() < self.nmf_red_size():
+            raise HsnctError(E_ARG, "red must be a float64 device tensor of nmf_red_size() values")
+        ws = self.workspace(OP_DECOMPOSE) if ws is None else ws
+        _check(lib().hsnct_nmf_rowpass(self._h, _ptr(Y), ld, _ptr(V), _ptr(D), int(it), _ptr(ws),
+                                       ws.numel() * ws.element_size(), _ptr(red), _stream(stream, self.device)))
+
+    def nmf_dupdate(self, D, red, it, obj2=None, ws=None, stream=None):
+        """D update of iteration `it` from the all-reduced sums (hsnct_nmf_dupdate)."""
+        self._dev(D, "D", (self.K, self.Nk))
+        ws = self.workspace(OP_DECOMPOSE) if ws is None else ws
+        _check(lib().hsnct_nmf_dupdate(self._h, _ptr(D), _ptr(red), int(it), _ptr(obj2), _ptr(ws),
+                                       ws.numel() * ws.element_size(), _stream(stream, self.device)))
 
     def fbp(self, V, X=None, ws=None, stream=None):
         """FBP of the K subspace sinograms -> X [K, N_r, N_c, N_c] (hsnct_fbp)."""
