@@ -56,6 +56,25 @@ __device__ __forceinline__ float2 ffma2s(float x, float2 b, float2 c) {
     return r;
 }
 
+// complex a + b and a - b as one packed f32x2 instruction each (FADD2): the butterflies' adds
+// are ~60% of the FFT's floating-point instructions
+__device__ __forceinline__ float2 cadd2(float2 a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+__device__ __forceinline__ float2 csub2(float2 a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+        "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -206,8 +225,8 @@ __device__ __forceinline__ void dft_reg(float2 (&x)[N]) {
                 const float2 b = (q == 0)       ? b0
                                  : (4 * q == N) ? (INV ? make_float2(-b0.y, b0.x) : make_float2(b0.y, -b0.x))
                                                 : cmul(tw, b0);
-                x[i0 + j] = make_float2(a.x + b.x, a.y + b.y);
-                x[i0 + j + m] = make_float2(a.x - b.x, a.y - b.y);
+                x[i0 + j] = cadd2(a, b);
+                x[i0 + j + m] = csub2(a, b);
             }
         }
     }
