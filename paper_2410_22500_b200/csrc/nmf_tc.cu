@@ -11,36 +11,28 @@
 // Why a cluster.  The V update needs all N_k bins of a row before phase 2 may use the new V,
 // so a tile's rows must stay on chip between the two phases; UMMA needs >= 64 rows, and 64 rows
 // x 1600 bins x 4 B = 410 KB exceeds one SM's shared memory.  A cluster of NCL = 4 CTAs splits
-// the bins into four ranges (the bin range of cluster rank j is fixed for the kernel); every
-// CTA streams its range of each tile into a ring of 128-bin chunk slots (64 rows x 128 bins),
-// computes its partial A in TMEM, the four partials are summed in a fixed rank order (pushed
-// to the peers with st.async; bitwise identical in all four CTAs), every CTA applies the same
-// V update, and phase 2 runs on the tile's data.
-//
-// Why TMEM holds the tile for phase 2.  Keeping the chunks in shared memory until phase 2
-// (round 2's first version) leaves room for two tiles, and the ~3 us between a tile's last
-// chunk landing and its phase-2 MMAs completing (cluster exchange, V update, MMAs) drained the
-// ring every tile (0.53 of HBM).  Here each chunk is stored in transposed
-// core-matrix order (8 rows of one bin contiguous): phase 1 reads it as an MN-major operand,
-// tcgen05.cp then copies it into TMEM with the bins on the 128 lanes -- exactly phase 2's A
-// operand (Y+^T, M = 128 bins, K = rows) -- and the shared-memory slot is free again.  TMEM
-// (512 columns) holds one tile's Y+^T (256) and the phase-1 / phase-2 accumulators (256).
+// the bins into four ranges (the lambda range of cluster rank j is fixed for the kernel); every
+// CTA streams its range of each tile into a ring of 16 KB chunk slots (64 rows x 64 bins),
+// computes its partial A in TMEM, the four partials are summed through distributed shared
+// memory in a fixed rank order (bitwise identical in all four CTAs), every CTA applies the
+// same V update, and phase 2 runs on its resident chunks.
 //
 // Precision (R20).  fp32-accurate products from an fp16 hi/lo split: x = hi + lo,
 // hi = fp16(s x), lo = fp16(s x - hi), |x - (hi + lo)/s| <= 2^-22 |x| for the scaled values in
 // the normal range, with power-of-two scales s chosen so that s*max < 2^14: one per call for Y+
-// (k_tc_stats), one per component and CTA range for D (kernel prologue), one per component
-// for V (the launch's Cauchy-Schwarz bound).  Each MMA uses [hi | lo] of the small operand as
-// its N = 16 columns, and the large operand's hi and lo are two MMAs into the same accumulator,
-// so all four partial products are summed.  Tensor-core accumulation truncates, which biases
-// long sums; every accumulator therefore covers one chunk (phase 1) or one tile (phase 2), and
-// the rest of the sums are fp32 FADD/FFMA in registers.
+// (k_tc_stats), one per component and CTA range for D (kernel prologue), one per component and
+// tile for V (the tile's own max).  Each MMA uses [hi | lo] of the small operand as its N = 16
+// columns, and the large operand's hi and lo are two MMAs into the same accumulator, so all
+// four partial products are summed exactly in fp32.  Tensor-core accumulation truncates, which
+// biases long sums; every accumulator therefore covers one 64-bin chunk (phase 1) or one tile
+// (phase 2) only, and the rest of the sums are fp32 FADD/FFMA in registers.
 //
-// Warps (256 threads, one CTA per SM): 0 producer (cp.async.bulk of each chunk), 1 phase-1 MMA
-// issuer + tcgen05.cp, 2 and 3 phase-2 MMA issuers (even / odd bin blocks), 4-7 epilogue (TMEM
-// drains, the A exchange, the V update, V in operand layout, B in fp32 registers, H = V^T V).
-// The issuers are whole converged warps (elect.sync inside the asm) so that descriptor math
-// stays warp-uniform: ~15-20 ns per MMA instead of ~60-80 from one divergent lane.
+// Warp roles (192 threads, one CTA per SM):
+//   warp 0   producer: cp.async.bulk of each chunk (hi and lo blocks, contiguous) into the ring
+//   warp 1   MMA issuer (one thread): phase 1 of tile i, phase 2 of tile i-1 as soon as its
+//            V is ready or a ring slot it holds is needed; tcgen05.commit releases the slots
+//   warps 2-5 epilogue: TMEM drains, the cluster exchange of A, the V update, V in its
+//            operand layout, the phase-2 drain into fp32 register accumulators of B, H = V^T V
 // Deterministic: static tile schedule, fixed-order sums, no floating-point atomics.
 #include <cuda_fp16.h>
 
@@ -58,15 +50,16 @@ using namespace tc;
 constexpr int TR = 64;                  // rows per tile (phase-1 UMMA M = 64)
 constexpr int NCL = TC_CLUSTER;         // CTAs per cluster = bin ranges
 constexpr int NN = 16;                  // UMMA N: [hi k = 0..7 | lo k = 0..7]
-constexpr int CW = 128;                 // bins per chunk = phase-2 M = TMEM lanes
-constexpr int MAXCH = 4;                // chunks per range (TMEM: 64 columns of Y+^T each)
-constexpr int NB = 16;                  // chunks in flight (mbarrier pairs of the byte ring)
-constexpr uint32_t COL_P1 = 256, COL_P2 = 384;  // TMEM: [0,256) Y+^T, P1 / P2 accumulators (2 parities)
+constexpr int MAXCH = 8;                // chunks per range
+constexpr int MAXR = 16;                // ring slots (upper bound)
 constexpr int VOPB = 8 * 2 * 128;       // bytes of the V operand (8 row groups x 2 n groups)
 constexpr int XRB = (NCL - 1) * TR * 8 * 4;  // bytes of the peers' partials of A (one tile)
+// Warps: 0 producer (one lane), 1 phase-1 MMA issuer, 2 and 3 phase-2 MMA issuers (even / odd
+// chunks; whole converged warps, elect.sync inside the MMA asm: ~15-20 ns per MMA), 4-7
+// epilogue (TMEM lane quarter = warp % 4).  Two warps per SM sub-partition leave 255 registers.
 constexpr int NTHR = 256;
 constexpr int EPI0 = 128;               // first epilogue thread
-constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t TMEM_COLS = 512;     // [0, 256): phase-1 accumulators, [256, 512): phase 2
 
 struct TcArgs {
     const __half* Yc;       // converted Y+: [tile][range][chunk][hi | lo][row group][bin group][8][8]
@@ -82,7 +75,10 @@ struct TcArgs {
     const unsigned* ynorm;  // bits of max_r ||Y+_r||^2 (k_tc_stats)
     unsigned* status;
     int first;
-    int R;                  // bytes of the chunk ring (chunks packed at their real size, FIFO)
+    int R;                  // ring slots (phase 1; shared with phase 2 when R2 == 0)
+    int R2;                 // phase-2 ring slots: 0 = phase 2 reads the phase-1 ring (chunks stay
+                            // resident through the V update); > 0 = phase 2 re-streams each tile's
+                            // chunks (from L2) into its own ring
     int maxch;              // chunks of the longest range (D-operand buffer)
     TcRanges rg;
     uint64_t* trace;        // diagnostics: [tile][nCTA][TRACE_SLOTS] %globaltimer stamps, or null
@@ -131,9 +127,8 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
     static_assert(K >= 1 && K <= 8, "tcgen05 pass: K <= 8");
     constexpr int KK = K * K;
     extern __shared__ __align__(1024) uint8_t sm[];
-    __shared__ uint64_t full[NB], empty[NB];
-    __shared__ uint32_t choff[NB];      // byte offset in the ring of the chunk using barrier pair b
-    __shared__ uint64_t ydone, yfree;   // tile's Y+^T copied into TMEM / phase 2 done reading it
+    __shared__ uint64_t full[MAXR], empty[MAXR], full2[MAXR], empty2[MAXR];
+    __shared__ volatile int p1seen;     // tiles whose phase-1 chunks have all landed (re-stream mode)
     __shared__ uint64_t p1full[2], p1empty[2], vfull[2], p2full[2], p2empty[2], xfull, xempty;
     __shared__ uint32_t tbase;
     __shared__ double Gs[KK];
@@ -153,10 +148,12 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
     const uint32_t cid = cluster_id(), ncl = num_clusters();
     const int W = A.rg.W;
     const int l0 = A.rg.l0[rank], L = A.rg.L[rank], nch = A.rg.nch[rank];
-    const uint32_t RB = (uint32_t)A.R;  // ring bytes
+    const int R = A.R, R2 = A.R2;
+    const int SLOTB = TR * W * 4;       // one chunk: hi + lo halves
     const int DOPC = W * 32;            // one chunk of the D operand: W/8 bin groups x 2 n groups x 128 B
     uint8_t* ring = sm;
-    uint8_t* Dop = sm + RB;             // (the tail chunk's TMEM copy may read past the ring into Dop)
+    uint8_t* ring2 = sm + (size_t)R * SLOTB;
+    uint8_t* Dop = ring2 + (size_t)R2 * SLOTB;
     uint8_t* Vop = Dop + (size_t)A.maxch * DOPC;
     float* xrecv = reinterpret_cast<float*>(Vop + 2 * VOPB);  // [NCL-1][TR][8] partials of A from the peers
     const int64_t ntiles = (A.Np + TR - 1) / TR;
@@ -164,17 +161,20 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
 
     // ---------------------------------------------------------------- prologue
     if (tid == 0) {
-        for (int s = 0; s < NB; ++s) {
+        for (int s = 0; s < R; ++s) {
             mb_init(&full[s], 1);
             mb_init(&empty[s], 1);
         }
-        mb_init(&ydone, 1);
-        mb_init(&yfree, 2);  // one commit per phase-2 issuer
+        for (int s = 0; s < R2; ++s) {
+            mb_init(&full2[s], 1);
+            mb_init(&empty2[s], 1);
+        }
+        p1seen = 0;
         for (int b = 0; b < 2; ++b) {
             mb_init(&p1full[b], 1);
             mb_init(&p1empty[b], 4);
             mb_init(&vfull[b], 1);
-            mb_init(&p2full[b], 2);   // one commit per phase-2 issuer
+            mb_init(&p2full[b], R2 ? 1 : 2);   // one commit per phase-2 issuer
             mb_init(&p2empty[b], 4);
         }
         mb_init(&xfull, 1);          // armed by expect_tx; completed by the peers' st.async bytes
@@ -229,122 +229,108 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
-        // Byte ring: chunks (32 KB, and the range's short tail) are packed FIFO at their real
-        // size, so the ring holds two whole tiles; a chunk is released (empty[b]) once its
-        // phase-1 MMAs and its copy into TMEM have completed, in order.
         if (lane == 0) {
-            const uint64_t pol = policy_evict_first();  // streamed once per iteration
-            uint32_t start[NB];                         // ring offset of the in-flight chunks
-            uint32_t head = 0;
-            int64_t seq = 0, oldest = 0;                // oldest chunk not yet known to be released
-            auto release_oldest = [&]() {
-                mb_wait(&empty[oldest % NB], (unsigned)((oldest / NB) & 1));
-                ++oldest;
-            };
+            // streamed once: evict first; re-streamed by phase 2 from L2: default (LRU) policy
+            const uint64_t pol = R2 ? policy_evict_normal() : policy_evict_first();
+            int64_t seq = 0;
             for (int64_t i = 0; i < nmine; ++i) {
                 const int64_t t = cid + i * ncl;
                 for (int c = 0; c < nch; ++c, ++seq) {
-                    const uint32_t bytes = 2048u * (uint32_t)chunk_groups(L, c, W);
-                    uint32_t at;
-                    for (;;) {
-                        if (seq - oldest >= NB) {
-                            release_oldest();
-                            continue;
-                        }
-                        if (oldest == seq) head = 0;  // ring empty: restart at its base
-                        const uint32_t tail = oldest < seq ? start[oldest % NB] : head;
-                        if (oldest == seq || head > tail) {  // free: [head, RB) and [0, tail)
-                            if (head + bytes <= RB) { at = head; break; }
-                            if (bytes <= tail) { at = 0; break; }
-                        } else if (head + bytes <= tail) {   // free: [head, tail)
-                            at = head;
-                            break;
-                        }
-                        release_oldest();
-                    }
-                    start[seq % NB] = at;
-                    head = at + bytes;
-                    const int b = (int)(seq % NB);
+                    const int s = (int)(seq % R);
+                    mb_wait(&empty[s], (unsigned)(((seq / R) & 1) ^ 1));
                     if (c == 0) stamp(i, TS_LD_0);
                     if (c == nch - 1) stamp(i, TS_LD_END);
-                    choff[b] = at;  // published to the consumers by the expect_tx arrive (release)
-                    mb_expect_tx(&full[b], bytes);
-                    bulk_g2s_hint(ring + at, A.Yc + chunk_off(t, A.Nk16, l0, c, W), bytes, &full[b], pol);
+                    const unsigned bytes = 2048u * (unsigned)chunk_groups(L, c, W);
+                    mb_expect_tx(&full[s], bytes);
+                    bulk_g2s_hint(ring + (size_t)s * SLOTB, A.Yc + chunk_off(t, A.Nk16, l0, c, W), bytes, &full[s], pol);
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ phase-1 MMA issuer + copy to TMEM
-        constexpr uint32_t ID1 = idesc_f16(64, NN, true);  // A = Y+ tile (64 rows), MN-major (rows contiguous)
+        // ------------------------------------------------------------ phase-1 MMA issuer (whole warp)
+        constexpr uint32_t ID1 = idesc_f16(64, NN, false);  // A = Y+ tile (64 rows), K-major over bins
         const uint32_t ring_a = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
         const uint32_t dop_a = __shfl_sync(0xffffffffu, smem_u32(Dop), 0);
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+        int64_t seq = 0;
         for (int64_t i = 0; i < nmine; ++i) {
             const int p = (int)(i & 1);
             if (i >= 2) mb_wait(&p1empty[p], (unsigned)(((i - 2) >> 1) & 1));
             fence_after();
-            for (int c = 0; c < nch; ++c) {
-                const int64_t seq = i * nch + c;
-                const int s = (int)(seq % NB);
-                mb_wait(&full[s], (unsigned)((seq / NB) & 1));
+            for (int c = 0; c < nch; ++c, ++seq) {
+                const int s = (int)(seq % R);
+                mb_wait(&full[s], (unsigned)((seq / R) & 1));
                 fence_after();
                 if (c == 0 && lane == 0) stamp(i, TS_MMA_P1_0);
                 const uint32_t w = (uint32_t)chunk_groups(L, c, W);
-                const uint32_t a = ring_a + choff[s];
-                const uint32_t d = tm + COL_P1 + (uint32_t)p * 64u + (uint32_t)c * NN;
-                // MN-major A: LBO = bin-group stride (K), SBO = row-group stride (M); K-step = 2 bin groups
-                const uint64_t ah = sdesc(a, 1024u, 128u), al = sdesc(a + 1024u * w, 1024u, 128u);
+                const uint32_t a = ring_a + (uint32_t)s * SLOTB;
+                const uint32_t d = tm + (uint32_t)p * 128u + (uint32_t)c * NN;
+                const uint64_t ah = sdesc(a, 128u, w * 128u), al = sdesc(a + 1024u * w, 128u, w * 128u);
                 const uint64_t bd = sdesc(dop_a + (uint32_t)c * DOPC, 256u, 128u);
+                // descriptor start addresses advance in 16-byte units: +256 B (A), +512 B (B) per K-step
                 for (uint32_t ks = 0; ks < w / 2; ++ks) {
-                    mma_f16_warp(d, ah + ks * 128u, bd + ks * 32u, ID1, ks > 0 ? 1u : 0u);
-                    mma_f16_warp(d, al + ks * 128u, bd + ks * 32u, ID1, 1u);
+                    mma_f16_warp(d, ah + ks * 16u, bd + ks * 32u, ID1, ks > 0 ? 1u : 0u);
+                    mma_f16_warp(d, al + ks * 16u, bd + ks * 32u, ID1, 1u);
                 }
+                if (R2) mma_commit_warp(&empty[s]);  // phase 2 re-streams: free the slot now
             }
+            if (R2 && lane == 0) p1seen = (int)(i + 1);  // every chunk of tile i has landed (is in L2)
             mma_commit_warp(&p1full[p]);
             if (lane == 0) stamp(i, TS_MMA_P1_END);
-            // Y+^T of this tile into TMEM (after phase 2 of the previous tile has read its copy);
-            // every chunk is a 128-bin block: 4 row blocks x (hi, lo) copies of 128 lanes x 256 bits
-            if (i >= 1) mb_wait(&yfree, (unsigned)((i - 1) & 1));
-            fence_after();
-            for (int c = 0; c < nch; ++c) {
-                const int64_t seq = i * nch + c;
-                const int s = (int)(seq % NB);
-                const uint32_t w = (uint32_t)chunk_groups(L, c, W);
-                const uint32_t a = ring_a + choff[s];
-#pragma unroll
-                for (uint32_t hl = 0; hl < 2; ++hl)
-#pragma unroll
-                    for (uint32_t kb = 0; kb < TR / 16; ++kb)
-                        tmem_cp_128x256b_warp(tm + (uint32_t)c * 64u + hl * 32u + kb * 8u,
-                                              sdesc(a + hl * 1024u * w + kb * 256u, 128u, 1024u));
-                mma_commit_warp(&empty[s]);  // the slot is free once its MMAs and copies completed
+        }
+    } else if (warp == 3 && R2) {
+        // ------------------------------------------------------------ phase-2 re-stream producer
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();  // second and last read of these bytes
+            int64_t seq = 0;
+            for (int64_t i = 0; i < nmine; ++i) {
+                while (p1seen <= (int)i) __nanosleep(64);
+                const int64_t t = cid + i * ncl;
+                for (int c = 0; c < nch; ++c, ++seq) {
+                    const int s = (int)(seq % R2);
+                    mb_wait(&empty2[s], (unsigned)(((seq / R2) & 1) ^ 1));
+                    const unsigned bytes = 2048u * (unsigned)chunk_groups(L, c, W);
+                    mb_expect_tx(&full2[s], bytes);
+                    bulk_g2s_hint(ring2 + (size_t)s * SLOTB, A.Yc + chunk_off(t, A.Nk16, l0, c, W), bytes, &full2[s], pol);
+                }
             }
-            mma_commit_warp(&ydone);
         }
     } else if (warp == 2 || warp == 3) {
-        // ------------------------------------------------------------ phase-2 MMA issuers (A = Y+^T in TMEM)
-        constexpr uint32_t ID2 = idesc_f16(128, NN, false);  // A from TMEM: 128 bins x 16 rows per MMA
+        // ------------------------------------------------------------ phase-2 MMA issuers (whole warps)
+        constexpr uint32_t ID2 = idesc_f16(128, NN, true);  // A = Y+ tile^T (128 bins), MN-major
+        const uint32_t ring_a = __shfl_sync(0xffffffffu, smem_u32(ring), 0);
         const uint32_t vop_a = __shfl_sync(0xffffffffu, smem_u32(Vop), 0);
+        const uint32_t ring2_a = __shfl_sync(0xffffffffu, smem_u32(ring2), 0);
         const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
-        const int c0 = warp - 2;  // bin blocks of this issuer: even / odd
+        const int c0 = warp - 2;           // chunk parity of this issuer (two issuers when resident)
+        const int cstep = R2 ? 1 : 2;      // one issuer (warp 2) when phase 2 re-streams
         for (int64_t i = 0; i < nmine; ++i) {
             const int p = (int)(i & 1);
             mb_wait(&vfull[p], (unsigned)((i >> 1) & 1));
-            mb_wait(&ydone, (unsigned)(i & 1));
             if (i >= 2) mb_wait(&p2empty[p], (unsigned)(((i - 2) >> 1) & 1));
             fence_after();
             if (lane == 0 && c0 == 0) stamp(i, TS_MMA_P2_0);
             const uint64_t vb = sdesc(vop_a + (uint32_t)p * VOPB, 256u, 128u);
-            for (int c = c0; c < nch; c += 2) {
-                const uint32_t d = tm + COL_P2 + (uint32_t)p * 64u + (uint32_t)c * NN;
+            for (int c = c0; c < nch; c += cstep) {
+                const int64_t seq = i * nch + c;
+                const int s = (int)(seq % (R2 ? R2 : R));
+                if (R2) {
+                    mb_wait(&full2[s], (unsigned)((seq / R2) & 1));
+                    fence_after();
+                }
+                const uint32_t w = (uint32_t)chunk_groups(L, c, W);
+                const uint32_t a = (R2 ? ring2_a : ring_a) + (uint32_t)s * SLOTB;
+                const uint32_t d = tm + 256u + (uint32_t)p * 128u + (uint32_t)c * NN;
+                const uint64_t ah = sdesc(a, w * 128u, 128u), al = sdesc(a + 1024u * w, w * 128u, 128u);
+                const uint32_t kst = (2u * w * 128u) >> 4;  // K-step (16 rows = 2 row groups), 16-B units
 #pragma unroll
                 for (uint32_t ks = 0; ks < TR / 16; ++ks) {
-                    mma_f16_tmem_warp(d, tm + (uint32_t)c * 64u + ks * 8u, vb + ks * 32u, ID2, ks > 0 ? 1u : 0u);
-                    mma_f16_tmem_warp(d, tm + (uint32_t)c * 64u + 32u + ks * 8u, vb + ks * 32u, ID2, 1u);
+                    mma_f16_warp(d, ah + ks * kst, vb + ks * 32u, ID2, ks > 0 ? 1u : 0u);
+                    mma_f16_warp(d, al + ks * kst, vb + ks * 32u, ID2, 1u);
                 }
+                mma_commit_warp(R2 ? &empty2[s] : &empty[s]);  // the slot is free once these MMAs have read it
             }
             mma_commit_warp(&p2full[p]);
-            mma_commit_warp(&yfree);
             if (lane == 0 && c0 == 0) stamp(i, TS_MMA_P2_END);
         }
     } else if (warp >= 4 && warp < 8) {
@@ -355,7 +341,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
         const int row = 16 * q + lane;
         const uint32_t toff = tmem + ((uint32_t)(32 * q) << 16);
         constexpr int KT = K * (K + 1) / 2;  // upper triangle of H
-        float bacc[MAXCH][K];                // B partial: bin l0 + c CW + 32 q + lane (phase-2 M = 128 lanes)
+        float bacc[MAXCH][K];                // B partial: bin l0 + c W + 32 q + lane (phase-2 M = 128 lanes)
 #pragma unroll
         for (int c = 0; c < MAXCH; ++c)
 #pragma unroll
@@ -381,7 +367,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
             for (int c0 = 0; c0 < MAXCH; c0 += 2) {
                 if (c0 < nch) {
                     float v[32];
-                    tmem_ld32(toff + COL_P2 + (uint32_t)pp * 64u + (uint32_t)c0 * NN, v);
+                    tmem_ld32(toff + 256u + (uint32_t)pp * 128u + (uint32_t)c0 * NN, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
@@ -396,17 +382,15 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
             __syncwarp();
             if (lane == 0) mb_arrive(&p2empty[pp]);
         };
-        // V_old prefetched two tiles ahead: under full HBM load a global read takes ~3 us, about
-        // one tile period, so a one-tile prefetch left the V update waiting on it
-        float vold[K], vnext[K];
-        auto load_v = [&](int64_t i, float (&dst)[K]) {
+        // V_old of the next tile, prefetched one tile ahead (its latency is off the chain)
+        float vold[K];
+        auto load_vold = [&](int64_t i) {
             const int64_t grow = (cid + i * ncl) * TR + row;
             const bool valid = act && i < nmine && grow < A.Np;
 #pragma unroll
-            for (int k = 0; k < K; ++k) dst[k] = valid ? __ldcg(A.V + grow * K + k) : 0.f;
+            for (int k = 0; k < K; ++k) vold[k] = valid ? __ldcg(A.V + grow * K + k) : 0.f;
         };
-        load_v(0, vold);
-        load_v(1, vnext);
+        load_vold(0);
         for (int64_t i = 0; i < nmine; ++i) {
             const int p = (int)(i & 1);
             const int64_t t = cid + i * ncl;
@@ -429,7 +413,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
             for (int c0 = 0; c0 < MAXCH; c0 += 2) {
                 if (c0 < nch) {
                     float v[32];
-                    tmem_ld32(toff + COL_P1 + (uint32_t)p * 64u + (uint32_t)c0 * NN, v);
+                    tmem_ld32(toff + (uint32_t)p * 128u + (uint32_t)c0 * NN, v);
                     tmem_ld_wait();
 #pragma unroll
                     for (int u = 0; u < 2; ++u)
@@ -510,9 +494,7 @@ __global__ void __launch_bounds__(NTHR, 1) k_nmf_tc(TcArgs A) {
                     vop[64 + k * 8] = lo;
                 }
             }
-#pragma unroll
-            for (int k = 0; k < K; ++k) vold[k] = vnext[k];
-            load_v(i + 2, vnext);
+            load_vold(i + 1);
             fence_proxy_async();
             named_bar(1, 128);
             if (e == 0) {
@@ -652,12 +634,9 @@ __global__ void __launch_bounds__(256) k_tc_stats(const float* __restrict__ Y, i
     }
 }
 
-// Pass 2: Y+ scaled by sigma_Y and split into fp16 hi/lo, per chunk in TRANSPOSED core-matrix
-// order: [hi | lo][bin group lg][row group rg][8 bins][8 rows] (8 consecutive tile rows of one
-// bin are 16 contiguous bytes).  Phase 1 reads a chunk as an MN-major operand (M = rows) and
-// tcgen05.cp copies it into TMEM with the bins on the lanes (phase 2's A = Y+^T).
-// Item (tile t, row group rg, global bin group G, bin l8), l8 fastest: a warp reads 32
-// consecutive bins of each of 8 rows (coalesced) and writes 16 bytes per thread.
+// Pass 2: Y+ scaled by sigma_Y and split into fp16 hi/lo in the chunked UMMA core-matrix layout.
+// Item (tile t, row group rg, bin group g, row rr), rr fastest: 8 consecutive threads write one
+// 128-byte core matrix row block (coalesced), each reading 8 bins of its row.
 __global__ void __launch_bounds__(256) k_tc_convert(const float* __restrict__ Y, int64_t ld, int64_t Np, int Nk,
                                                     int Nk16, TcRanges rg, const unsigned* __restrict__ ymax,
                                                     __half* __restrict__ Yc) {
@@ -666,24 +645,31 @@ __global__ void __launch_bounds__(256) k_tc_convert(const float* __restrict__ Y,
     const int64_t ntiles = (Np + TR - 1) / TR;
     const int64_t n = ntiles * 8 * G8 * 8;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int l8 = (int)(i & 7);
+        const int rr = (int)(i & 7);
         int64_t u = i >> 3;
-        const int G = (int)(u % G8);
+        const int g = (int)(u % G8);
         u /= G8;
         const int rgi = (int)(u & 7);
         const int64_t t = u >> 3;
-        const int l = G * 8 + l8;
-        const int64_t r0 = t * TR + rgi * 8;
+        const int64_t r = t * TR + rgi * 8 + rr;
+        const int l = g * 8;
         float v[8];
+        if (r < Np && l + 8 <= Nk) {
+            const float4* y = reinterpret_cast<const float4*>(Y + r * ld + l);
+            const float4 a = __ldg(y), b = __ldg(y + 1);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
 #pragma unroll
-        for (int r8 = 0; r8 < 8; ++r8) v[r8] = (r0 + r8 < Np && l < Nk) ? __ldg(Y + (r0 + r8) * ld + l) : 0.f;
+            for (int j = 0; j < 8; ++j) v[j] = (r < Np && l + j < Nk) ? Y[r * ld + l + j] : 0.f;
+        }
         // bin range j, chunk c, bin group within the chunk
         int j = 0;
 #pragma unroll
         for (int jj = 1; jj < NCL; ++jj)
             if (l >= rg.l0[jj]) j = jj;
         const int loc = l - rg.l0[j];
-        const int c = loc / rg.W, lg = (loc - c * rg.W) >> 3;
+        const int c = loc / rg.W, lb = (loc - c * rg.W) >> 3;
         const int w = chunk_groups(rg.L[j], c, rg.W);
         uint32_t hw[4], lw[4];
 #pragma unroll
@@ -694,14 +680,14 @@ __global__ void __launch_bounds__(256) k_tc_convert(const float* __restrict__ Y,
             hw[q] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
             lw[q] = (uint32_t)__half_as_ushort(l0_) | ((uint32_t)__half_as_ushort(l1) << 16);
         }
-        __half* dst = Yc + chunk_off(t, Nk16, rg.l0[j], c, rg.W) + (int64_t)((lg * 8 + rgi) * 8 + l8) * 8;
+        __half* dst = Yc + chunk_off(t, Nk16, rg.l0[j], c, rg.W) + (int64_t)((rgi * w + lb) * 8 + rr) * 8;
         *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
         *reinterpret_cast<uint4*>(dst + 512 * w) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
 }
 
-size_t tc_smem_bytes(int ring_bytes, int W, int maxch) {
-    return (size_t)ring_bytes + (size_t)maxch * W * 32 + 2 * VOPB + XRB;
+size_t tc_smem_bytes(int R, int W, int maxch) {  // R: all ring slots (phase 1 + phase 2)
+    return (size_t)R * TR * W * 4 + (size_t)maxch * W * 32 + 2 * VOPB + XRB;
 }
 
 template <int K>
@@ -727,6 +713,7 @@ cudaError_t tc_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, flo
     A.status = status;
     A.first = it == 0 ? 1 : 0;
     A.R = p.tc_R;
+    A.R2 = p.tc_R2;
     A.maxch = p.tc_maxch;
     A.rg = p.tc_rg;
     A.trace = w.trace;
@@ -788,14 +775,26 @@ bool nmf_tc_plan(const Geometry& g, int num_sms, NmfPlan* p) {
         acc += cnt;
         Lmax = std::max(Lmax, rg.L[j]);
     }
-    // 128-bin chunks: one chunk = one block of 128 TMEM lanes of Y+^T
-    const size_t budget = (size_t)232448 - 3072;  // 227 KB minus the driver's 1 KB and <= 2 KB static
-    const int bestW = CW;
-    const int maxch0 = (Lmax + CW - 1) / CW;
-    if (maxch0 > MAXCH) return false;
-    // the rest of the shared memory is the byte ring (16-byte granular); it must hold a tile
-    const int bestR = (int)((budget - tc_smem_bytes(0, bestW, maxch0)) & ~(size_t)15);
-    if (bestR < maxch0 * TR * CW * 4) return false;
+    // chunk width: the one whose ring holds the most whole tiles of the longest range (the
+    // ring must hold one tile while the next streams in)
+    // 227 KB per block minus the driver's 1 KB and at most 2 KB of static shared memory
+    const size_t budget = (size_t)232448 - 3072;
+    int bestW = 0, bestR = 0;
+    double best = 0.0;
+    for (int W = 64; W <= 128; W += 16) {
+        const int nch = (Lmax + W - 1) / W;
+        if (nch > MAXCH) continue;
+        int R = MAXR;
+        while (R > 0 && tc_smem_bytes(R, W, nch) > budget) --R;
+        if (R < nch + 1) continue;
+        const double depth = (double)R / nch;
+        if (depth > best + 1e-9) {
+            best = depth;
+            bestW = W;
+            bestR = R;
+        }
+    }
+    if (!bestW) return false;
     rg.W = bestW;
     int maxch = 0;
     for (int j = 0; j < NCL; ++j) {
@@ -815,8 +814,14 @@ bool nmf_tc_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const int64_t ntiles = (Np + TR - 1) / TR;
     p->tc_ncl = (int)std::max<int64_t>(1, std::min<int64_t>(ncl, ntiles));
-    p->tc_R = bestR;
-    p->tc_R2 = 0;
+    // Default: each tile's chunks stay resident in one ring through the V update.
+    // HSNCT_TC_RESTREAM=1: phase 2 re-streams them from L2 into a second ring (the phase-1 ring
+    // takes half the slots rounded up); measured slower (L2 latency doubles under the 2x L2
+    // traffic)
+    const char* rs = getenv("HSNCT_TC_RESTREAM");
+    const bool restream = rs && rs[0] == '1' && bestR - (bestR + 1) / 2 >= maxch;
+    p->tc_R = restream ? (bestR + 1) / 2 : bestR;
+    p->tc_R2 = restream ? bestR - p->tc_R : 0;
     p->tc_maxch = maxch;
     p->tc_smem = smem;
     p->tc_rg = rg;
