@@ -66,6 +66,18 @@ def lib():
             L.oracle_backproject_slice.argtypes = [_f64p, _i64, _i64, _f64p, _f64p]
             L.oracle_splat_project_slice.restype = None
             L.oracle_splat_project_slice.argtypes = [_f64p, _i64, _i64, _f64p, _f64p]
+            L.oracle_qggmrf_rho.restype = ctypes.c_double
+            L.oracle_qggmrf_rho.argtypes = [ctypes.c_double, _f64p]
+            L.oracle_qggmrf_omega.restype = ctypes.c_double
+            L.oracle_qggmrf_omega.argtypes = [ctypes.c_double, _f64p]
+            L.oracle_mbir_project_slice.restype = None
+            L.oracle_mbir_project_slice.argtypes = [_f64p, _i64, _i64, _f64p, _f64p]
+            L.oracle_mbir_backproject_slice.restype = None
+            L.oracle_mbir_backproject_slice.argtypes = [_f64p, _i64, _i64, _f64p, _f64p]
+            L.oracle_mbir_slice.restype = _int
+            L.oracle_mbir_slice.argtypes = [_f64p, _i64, _i64, _f64p, _f64p, _int, _f64p, _f64p]
+            L.oracle_mbir.restype = _int
+            L.oracle_mbir.argtypes = [_f64p, _i64, _i64, _i64, _int, _f64p, _f64p, _int, _f64p, _int]
             L.oracle_radon_naive.restype = None
             L.oracle_radon_naive.argtypes = [_f64p, _i64, _i64, _f64p, ctypes.c_double, _f64p, _int]
             L.oracle_fbp.restype = _int
@@ -299,3 +311,64 @@ def fmd_spectra(D, T):
     Dm = np.zeros((T.shape[0], D.shape[1]))
     lib().oracle_fmd_spectra(_p64(D), D.shape[1], D.shape[0], _p64(T), T.shape[0], _p64(Dm))
     return Dm
+
+
+# ------------------------------------------------------------------ MBIR (NEXT-3)
+def mbir_params(sigma_v, sigma_x, p=1.2, q=2.0, T=1.0):
+    """{sv, sx, p, q, T} of oracle.c's Eq. 5 objective (R24-R26)."""
+    return np.array([sigma_v, sigma_x, p, q, T], dtype=np.float64)
+
+
+def qggmrf_rho(d, prm):
+    return float(lib().oracle_qggmrf_rho(float(d), _p64(np.asarray(prm, np.float64))))
+
+
+def qggmrf_omega(d, prm):
+    return float(lib().oracle_qggmrf_omega(float(d), _p64(np.asarray(prm, np.float64))))
+
+
+def mbir_project_slice(X, nv, angles=None):
+    """(A x)[v][c] = sum_ij x_ij max(0, 1 - |u_ij(v) - c|) -> [nv, Nc]."""
+    X = _f64(X)
+    nc = X.shape[0]
+    a, ap = _angles(angles)
+    P = np.zeros((nv, nc))
+    lib().oracle_mbir_project_slice(_p64(X), nv, nc, ap, _p64(P))
+    return P
+
+
+def mbir_backproject_slice(R, angles=None):
+    """A^T r -> [Nc, Nc]."""
+    R = _f64(R)
+    nv, nc = R.shape
+    a, ap = _angles(angles)
+    X = np.zeros((nc, nc))
+    lib().oracle_mbir_backproject_slice(_p64(R), nv, nc, ap, _p64(X))
+    return X
+
+
+def mbir_slice(y, x0, prm, n_iter, angles=None, objective=False):
+    """SQS iterations of Eq. 5 on one slice: y [Nv, Nc], x0 [Nc, Nc] -> x (and the objective
+    of iterates 0..n_iter)."""
+    y = _f64(y)
+    nv, nc = y.shape
+    x = _f64(x0).copy()
+    a, ap = _angles(angles)
+    obj = np.zeros(n_iter + 1) if objective else None
+    rc = lib().oracle_mbir_slice(_p64(y), nv, nc, ap, _p64(np.asarray(prm, np.float64)), int(n_iter), _p64(x),
+                                 _p64(obj) if objective else None)
+    if rc:
+        raise ValueError("oracle_mbir_slice: bad parameters (q must be 2, p in [1, 2], sv, sx, T > 0)")
+    return (x, obj) if objective else x
+
+
+def mbir(V, Nv, Nr, Nc, X0, prm, n_iter, angles=None, nthreads=0):
+    """V [Np, K] subspace views, X0 [K, Nr, Nc, Nc] -> X after n_iter SQS iterations per channel/slice."""
+    V = _f64(V)
+    K = V.shape[1]
+    X = _f64(X0).copy()
+    a, ap = _angles(angles)
+    if lib().oracle_mbir(_p64(V), Nv, Nr, Nc, K, ap, _p64(np.asarray(prm, np.float64)), int(n_iter), _p64(X),
+                         int(nthreads)):
+        raise ValueError("oracle_mbir: bad parameters")
+    return X

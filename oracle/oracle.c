@@ -590,3 +590,157 @@ void oracle_fmd_spectra(const double* D, int64_t Nk, int K, const double* T, int
             Dm[(int64_t)i * Nk + l] = s;
         }
 }
+
+/* ------------------------------------------------------------------ MBIR (NEXT-3)
+ * Eq. 5 for one subspace channel of one slice:
+ *   x = argmin_{x >= 0} 1/(2 sv^2) ||y - A x||^2 + h(x),
+ * A the linear projection operator: (A x)[v][c] = sum_{i,j} x[i][j] max(0, 1 - |u_ij(v) - c|),
+ * u_ij(v) = x_j cos(theta_v) + y_i sin(theta_v) + (Nc-1)/2 (readings R13, R14, R16; the exact
+ * adjoint of the backprojector without its pi/Nv factor), h the QGGMRF prior (
+ * the pairwise form of SPEC.md:199 with q = 2, reading R24):
+ *   h(x) = sum over unordered 8-neighbour pairs {i, j} of b_ij rho(x_i - x_j),
+ *   rho(d) = |d|^p / (p sx^p) * u / (1 + u),  u = |d / (T sx)|^(q - p),
+ *   b = b1 for edge neighbours, b1 / sqrt(2) for diagonal ones, 4 b1 + 4 b1/sqrt(2) = 1 (R25).
+ * Solver (reading R26): separable-quadratic-surrogate majorize-minimize iterations.  With
+ * w(d) = rho'(d) / d (the half-quadratic curvature, non-increasing in |d| for p <= q = 2):
+ *   dd[i] = (1/sv^2) (A^T A 1)[i]                                   (data curvature, A >= 0)
+ *   e = y - A x;  g[i] = -(1/sv^2) (A^T e)[i] + sum_{j in N(i)} b_ij rho'(x_i - x_j)
+ *   dp[i] = sum_{j in N(i)} 2 b_ij w(x_i - x_j)
+ *   x[i] <- max(0, x[i] - g[i] / (dd[i] + dp[i]))          (every voxel from the same x: Jacobi)
+ * so the objective is non-increasing at every iteration (majorization).  y: [Nv][Nc];
+ * x: [Nc][Nc], in: x0, out: the n_iter-th iterate; obj (nullable): [n_iter + 1] objective
+ * values of the iterates 0..n_iter.  prm = {sv, sx, p, q, T}; q must be 2 (w(0) finite). */
+static double qg_rho(double d, const double* prm) {
+    const double sx = prm[1], p = prm[2], q = prm[3], T = prm[4];
+    const double a = fabs(d);
+    if (a == 0.0) return 0.0;
+    const double u = pow(a / (T * sx), q - p);
+    return pow(a, p) / (p * pow(sx, p)) * u / (1.0 + u);
+}
+/* w(d) = rho'(d)/d = |d|^(p-2)/sx^p * u/(1+u) * (1 + (q-p)/(p (1+u))); with q = 2,
+ * |d|^(p-2) u = 1/(T sx)^(2-p), so w(d) = 1/(sx^p (T sx)^(2-p)) / (1+u) * (1 + (2-p)/(p(1+u))). */
+static double qg_omega(double d, const double* prm) {
+    const double sx = prm[1], p = prm[2], T = prm[4];
+    const double u = pow(fabs(d) / (T * sx), 2.0 - p);
+    return 1.0 / (pow(sx, p) * pow(T * sx, 2.0 - p)) / (1.0 + u) * (1.0 + (2.0 - p) / (p * (1.0 + u)));
+}
+double oracle_qggmrf_rho(double d, const double* prm) { return qg_rho(d, prm); }
+double oracle_qggmrf_omega(double d, const double* prm) { return qg_omega(d, prm); }
+
+void oracle_mbir_project_slice(const double* X, int64_t Nv, int64_t Nc, const double* angles, double* P) {
+    double half = 0.5 * (double)(Nc - 1);
+    for (int64_t t = 0; t < Nv * Nc; ++t) P[t] = 0.0;
+    for (int64_t v = 0; v < Nv; ++v) {
+        double th = view_angle(angles, v, Nv);
+        for (int64_t i = 0; i < Nc; ++i)
+            for (int64_t j = 0; j < Nc; ++j) {
+                double u = ((double)j - half) * cos(th) + ((double)i - half) * sin(th) + half;
+                double fl = floor(u), w = u - fl;
+                int64_t i0 = (int64_t)fl;
+                if (i0 >= 0 && i0 < Nc) P[v * Nc + i0] += (1.0 - w) * X[i * Nc + j];
+                if (i0 + 1 >= 0 && i0 + 1 < Nc) P[v * Nc + i0 + 1] += w * X[i * Nc + j];
+            }
+    }
+}
+void oracle_mbir_backproject_slice(const double* R, int64_t Nv, int64_t Nc, const double* angles, double* X) {
+    double half = 0.5 * (double)(Nc - 1);
+    for (int64_t i = 0; i < Nc; ++i)
+        for (int64_t j = 0; j < Nc; ++j) {
+            double acc = 0.0;
+            for (int64_t v = 0; v < Nv; ++v) {
+                double th = view_angle(angles, v, Nv);
+                double u = ((double)j - half) * cos(th) + ((double)i - half) * sin(th) + half;
+                double fl = floor(u), w = u - fl;
+                int64_t i0 = (int64_t)fl;
+                double a = (i0 >= 0 && i0 < Nc) ? R[v * Nc + i0] : 0.0;
+                double b = (i0 + 1 >= 0 && i0 + 1 < Nc) ? R[v * Nc + i0 + 1] : 0.0;
+                acc += (1.0 - w) * a + w * b;
+            }
+            X[i * Nc + j] = acc;
+        }
+}
+
+static const int NB_DI[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+static const int NB_DJ[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+
+static double mbir_objective(const double* y, const double* ax, int64_t Nv, int64_t Nc, const double* x,
+                             const double* prm, double b1) {
+    double data = 0.0, prior = 0.0;
+    for (int64_t t = 0; t < Nv * Nc; ++t) data += (y[t] - ax[t]) * (y[t] - ax[t]);
+    for (int64_t i = 0; i < Nc; ++i)
+        for (int64_t j = 0; j < Nc; ++j)
+            for (int n = 0; n < 8; ++n) {  /* each unordered pair once: neighbours after (i, j) */
+                int64_t i2 = i + NB_DI[n], j2 = j + NB_DJ[n];
+                if (i2 < 0 || i2 >= Nc || j2 < 0 || j2 >= Nc) continue;
+                if (i2 * Nc + j2 <= i * Nc + j) continue;
+                double b = (NB_DI[n] != 0 && NB_DJ[n] != 0) ? b1 / sqrt(2.0) : b1;
+                prior += b * qg_rho(x[i * Nc + j] - x[i2 * Nc + j2], prm);
+            }
+    return data / (2.0 * prm[0] * prm[0]) + prior;
+}
+
+int oracle_mbir_slice(const double* y, int64_t Nv, int64_t Nc, const double* angles, const double* prm,
+                      int n_iter, double* x, double* obj) {
+    if (prm[3] != 2.0 || prm[0] <= 0.0 || prm[1] <= 0.0 || prm[2] < 1.0 || prm[2] > 2.0 || prm[4] <= 0.0) return 1;
+    const double iv = 1.0 / (prm[0] * prm[0]);
+    const double b1 = 1.0 / (4.0 + 4.0 / sqrt(2.0));
+    int64_t n = Nc * Nc, m = Nv * Nc;
+    double* one = calloc((size_t)n, sizeof(double));
+    double* dd = malloc(sizeof(double) * n);
+    double* ax = malloc(sizeof(double) * m);
+    double* e = malloc(sizeof(double) * m);
+    double* g = malloc(sizeof(double) * n);
+    double* xn = malloc(sizeof(double) * n);
+    for (int64_t t = 0; t < n; ++t) one[t] = 1.0;
+    oracle_mbir_project_slice(one, Nv, Nc, angles, ax);
+    oracle_mbir_backproject_slice(ax, Nv, Nc, angles, dd);
+    for (int64_t t = 0; t < n; ++t) dd[t] *= iv;
+    for (int it = 0; it <= n_iter; ++it) {
+        oracle_mbir_project_slice(x, Nv, Nc, angles, ax);
+        if (obj) obj[it] = mbir_objective(y, ax, Nv, Nc, x, prm, b1);
+        if (it == n_iter) break;
+        for (int64_t t = 0; t < m; ++t) e[t] = y[t] - ax[t];
+        oracle_mbir_backproject_slice(e, Nv, Nc, angles, g);
+        for (int64_t i = 0; i < Nc; ++i)
+            for (int64_t j = 0; j < Nc; ++j) {
+                double gi = -iv * g[i * Nc + j], di = dd[i * Nc + j];
+                for (int k = 0; k < 8; ++k) {
+                    int64_t i2 = i + NB_DI[k], j2 = j + NB_DJ[k];
+                    if (i2 < 0 || i2 >= Nc || j2 < 0 || j2 >= Nc) continue;
+                    double b = (NB_DI[k] != 0 && NB_DJ[k] != 0) ? b1 / sqrt(2.0) : b1;
+                    double d = x[i * Nc + j] - x[i2 * Nc + j2], w = qg_omega(d, prm);
+                    gi += b * w * d;      /* rho'(d) = w(d) d */
+                    di += 2.0 * b * w;
+                }
+                double v = x[i * Nc + j] - gi / di;
+                xn[i * Nc + j] = v > 0.0 ? v : 0.0;
+            }
+        memcpy(x, xn, sizeof(double) * n);
+    }
+    free(one);
+    free(dd);
+    free(ax);
+    free(e);
+    free(g);
+    free(xn);
+    return 0;
+}
+
+/* MBIR of the K subspace sinograms (Algorithm 1 with Eq. 5 in place of FBP):
+ * V [Np][K] (row p = (v Nr + r) Nc + c), X [K][Nr][Nc][Nc] in: x0, out: x_n; every (channel,
+ * slice) independently (2-D prior, R25). */
+int oracle_mbir(const double* V, int64_t Nv, int64_t Nr, int64_t Nc, int K, const double* angles,
+                const double* prm, int n_iter, double* X, int nthreads) {
+    set_threads(nthreads);
+    int bad = 0;
+#pragma omp parallel for schedule(dynamic) reduction(| : bad)
+    for (int64_t kr = 0; kr < (int64_t)K * Nr; ++kr) {
+        int64_t k = kr / Nr, r = kr % Nr;
+        double* y = malloc(sizeof(double) * Nv * Nc);
+        for (int64_t v = 0; v < Nv; ++v)
+            for (int64_t c = 0; c < Nc; ++c) y[v * Nc + c] = V[((v * Nr + r) * Nc + c) * K + k];
+        bad |= oracle_mbir_slice(y, Nv, Nc, angles, prm, n_iter, X + (k * Nr + r) * Nc * Nc, NULL);
+        free(y);
+    }
+    return bad;
+}
