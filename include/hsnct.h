@@ -11,6 +11,9 @@
  *   and the paper's baseline:
  *     hsnct_dhr                  direct hyperspectral reconstruction, one FBP per
  *                                wavelength bin
+ *   and, in place of FBP, the paper's model-based reconstruction (NEXT-3):
+ *     hsnct_mbir                 Eq. 5, QGGMRF prior, SQS iterations
+ *     hsnct_project              the forward projector A of Eq. 5
  *   plus hsnct_fhr_host, the whole of Algorithm 1 on HOST buffers (the
  *   end-to-end entry point: host->device copy, the three stages, device->host).
  *
@@ -85,7 +88,9 @@ typedef enum {
     HSNCT_OP_FBP = 1,       /* hsnct_fbp                                   */
     HSNCT_OP_DHR = 2,       /* hsnct_dhr, any window (the minimum is used) */
     HSNCT_OP_FHR_HOST = 3,  /* hsnct_fhr_host                              */
-    HSNCT_OP_FMD = 4        /* hsnct_fmd_transform / hsnct_fmd_materials   */
+    HSNCT_OP_FMD = 4,       /* hsnct_fmd_transform / hsnct_fmd_materials   */
+    HSNCT_OP_MBIR = 5,      /* hsnct_mbir                                  */
+    HSNCT_OP_PROJECT = 6    /* hsnct_project                               */
 } hsnct_op;
 
 typedef struct {
@@ -160,6 +165,32 @@ hsnct_status hsnct_nmf_dupdate(hsnct_t h, float* D, const double* red, int it, d
  * (N_v, N_r, N_c), is ramp-filtered along c and backprojected into X[k].
  * X must not overlap V or ws. */
 hsnct_status hsnct_fbp(hsnct_t h, const float* V, float* X, void* ws, size_t ws_bytes, void* stream);
+
+/* Model-based reconstruction of the K subspace sinograms (NEXT-3; Eq. 5, PAPER.md:224-228,
+ * DESIGN.md R24-R26), every channel k and slice r independently:
+ *   x = argmin_{x >= 0} 1/(2 sigma_v^2) ||y - A x||^2 + h(x),   y = column k of V on slice r,
+ * A the linear-interpolation projector (the exact adjoint of hsnct_fbp's backprojector without
+ * its pi/N_v factor: (A x)[v][c] = sum_ij x[i][j] max(0, 1 - |u_ij(v) - c|)), h the QGGMRF prior
+ * on the 8-neighbourhood of the slice: h(x) = sum_{pairs} b_ij rho(x_i - x_j),
+ *   rho(d) = |d|^p / (p sigma_x^p) * u / (1 + u),  u = |d / (T sigma_x)|^(q - p),
+ *   b = 1/(4 + 4/sqrt 2) for edge neighbours, b / sqrt 2 for diagonal ones.
+ * Solver: n_iter Jacobi separable-quadratic-surrogate steps (monotone in the objective)
+ *   x <- max(0, x - grad / ((1/sigma_v^2) A^T A 1 + sum_j 2 b_ij w(x_i - x_j))),  w = rho'(d)/d.
+ * X [K][N_r][N_c][N_c]: in x0 (e.g. the FBP), out the n_iter-th iterate (unchanged if n_iter
+ * == 0).  obj_trace (device fp64, n_iter + 1 entries, nullable): the objective summed over
+ * channels and slices at iterates 0..n_iter.  Parameters: sigma_v > 0, sigma_x > 0,
+ * 1 <= p <= 2, q == 2, T > 0, else E_ARG.  Workspace: hsnct_workspace_bytes(h, HSNCT_OP_MBIR).
+ * X, V, obj_trace and ws must not overlap.  A non-finite iterate sets E_NUMERIC (hsnct_sync).
+ * fp32 arithmetic; the objective sums use fp64 atomics (order not fixed). */
+typedef struct {
+    double sigma_v, sigma_x, p, q, T;
+} hsnct_mbir_params;
+hsnct_status hsnct_mbir(hsnct_t h, const float* V, float* X, int n_iter, const hsnct_mbir_params* prm,
+                        double* obj_trace, void* ws, size_t ws_bytes, void* stream);
+
+/* Forward projection of Eq. 5: P = A X, P [N_p][K] in the layout of V (row (v N_r + r) N_c + c),
+ * X [K][N_r][N_c][N_c].  Workspace: hsnct_workspace_bytes(h, HSNCT_OP_PROJECT). */
+hsnct_status hsnct_project(hsnct_t h, const float* X, float* P, void* ws, size_t ws_bytes, void* stream);
 
 /* Subspace expansion, Eq. 6, x^h = x^s (D^s)^T, on a
  * window: Xh[n][b] = sum_k X[k][slice0*N_c*N_c + n] * D[k][bin0 + b].

@@ -101,6 +101,23 @@ int64_t Nx_of(const Geometry& g) { return (int64_t)g.Nr * g.Nc * g.Nc; }
 int kc_of(int K) { return K <= 8 ? K : 16; }
 int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
 
+// hsnct_mbir workspace: two iterates Xi [Nx][KP], residual E [Np][Kc] (the backprojector's Q
+// layout), G = (pi/Nv) A^T E [K][Nx], and for A^T A 1: G1 [Nc^2], the ones image [Nc^2][2], E1 [Nv Nc]
+struct MbirLayout {
+    size_t xa, e, gk, g1, ones, e1, total;
+};
+MbirLayout mbir_layout(const Geometry& g) {
+    MbirLayout L{};
+    L.xa = a256((size_t)g.Nr * g.Nc * g.Nc * mbir_kp(g.K) * sizeof(float));
+    L.e = a256((size_t)g.Nv * g.Nr * g.Nc * (g.K <= 8 ? g.K : 16) * sizeof(float));
+    L.gk = a256((size_t)g.K * g.Nr * g.Nc * g.Nc * sizeof(float));
+    L.g1 = a256((size_t)g.Nc * g.Nc * sizeof(float));
+    L.ones = a256((size_t)g.Nc * g.Nc * 2 * sizeof(float));
+    L.e1 = a256((size_t)g.Nv * g.Nc * sizeof(float));
+    L.total = 2 * L.xa + L.e + L.gk + L.g1 + L.ones + L.e1;
+    return L;
+}
+
 size_t fbp_ws(const Geometry& g) { return a256((size_t)Np_of(g) * kc_of(g.K) * sizeof(float)); }
 // Filtered sinograms of one slice for one chunk of dhr_kc bins.
 size_t dhr_ws_chunk_slice(const Geometry& g) { return (size_t)g.Nv * g.Nc * dhr_kc(g) * sizeof(float); }
@@ -341,6 +358,12 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     al((void**)&h->t.status, sizeof(unsigned));
     al((void**)&h->t.nclamp, sizeof(unsigned long long));
     al((void**)&h->t.counter, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
+    const MbirGroups mg = mbir_groups(g, cs.data(), sn.data());
+    h->t.mbir_ng = mg.ng;
+    h->t.mbir_vb = mg.vb;
+    al((void**)&h->t.mbir_groups, mg.table.size() * sizeof(int));
+    if (e == cudaSuccess)
+        e = cudaMemcpy(h->t.mbir_groups, mg.table.data(), mg.table.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaHostAlloc((void**)&h->status_host, sizeof(unsigned), cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaMemcpy(h->t.cos_t, cs.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->t.sin_t, sn.data(), g.Nv * sizeof(float), cudaMemcpyHostToDevice);
@@ -377,6 +400,7 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.status);
     cudaFree(h->t.nclamp);
     cudaFree(h->t.counter);
+    cudaFree(h->t.mbir_groups);
     cudaFree(h->trace);
     for (cudaEvent_t e : h->fbp_ev)
         if (e) cudaEventDestroy(e);
@@ -397,6 +421,8 @@ size_t hsnct_workspace_bytes(hsnct_t h, int op) {
         case HSNCT_OP_DHR: return a256(dhr_ws_per_slice(h->g));
         case HSNCT_OP_FHR_HOST: return fhr_layout(h->g, h->nmf).total;
         case HSNCT_OP_FMD: return fmd_ws_bytes(h->g);
+        case HSNCT_OP_MBIR: return mbir_layout(h->g).total;
+        case HSNCT_OP_PROJECT: return mbir_layout(h->g).xa;
         default: return 0;
     }
 }
@@ -792,6 +818,95 @@ hsnct_status hsnct_fmd_spectra(hsnct_t h, const float* D, const float* T, int n_
     DeviceGuard guard(h->device);
     CK(fmd_spectra(g, D, T, n_mat, Dm, (cudaStream_t)stream), "fmd_spectra");
     h->launches += 1;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_mbir(hsnct_t h, const float* V, float* X, int n_iter, const hsnct_mbir_params* prm,
+                        double* obj_trace, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_mbir");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "mbir: handle is NULL");
+    const Geometry& g = h->g;
+    if (!V || !X || !prm) return fail(HSNCT_E_ARG, "mbir: V, X or params is NULL");
+    if (!aligned(V, 4) || !aligned(X, 4)) return fail(HSNCT_E_ARG, "mbir: V, X must be 4-byte aligned");
+    if (obj_trace && !aligned(obj_trace, 8)) return fail(HSNCT_E_ARG, "mbir: obj_trace misaligned");
+    if (n_iter < 0) return fail(HSNCT_E_ARG, "mbir: n_iter=%d < 0", n_iter);
+    const MbirPrm P{prm->sigma_v, prm->sigma_x, prm->p, prm->q, prm->T};
+    if (!(std::isfinite(P.sigma_v) && P.sigma_v > 0) || !(std::isfinite(P.sigma_x) && P.sigma_x > 0) ||
+        !(P.p >= 1.0 && P.p <= 2.0) || P.q != 2.0 || !(std::isfinite(P.T) && P.T > 0))
+        return fail(HSNCT_E_ARG, "mbir: need sigma_v > 0, sigma_x > 0, 1 <= p <= 2, q == 2, T > 0");
+    const MbirLayout L = mbir_layout(g);
+    hsnct_status st;
+    if ((st = check_ws(ws, ws_bytes, L.total, "mbir"))) return st;
+    const Range rV = rng(V, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rX = rng(X, (size_t)Nx_of(g) * g.K * sizeof(float));
+    const Range rW = rng(ws, L.total);
+    const Range rO = rng(obj_trace, obj_trace ? (size_t)(n_iter + 1) * sizeof(double) : 0);
+    if (overlap(rV, rX) || overlap(rW, rX) || overlap(rW, rV) || overlap(rO, rX) || overlap(rO, rV) || overlap(rO, rW))
+        return fail(HSNCT_E_ARG, "mbir: V, X, obj_trace and workspace must not overlap");
+    DeviceGuard guard(h->device);
+    const cudaStream_t s = (cudaStream_t)stream;
+    char* w = static_cast<char*>(ws);
+    float* Xa = reinterpret_cast<float*>(w);
+    float* Xb = reinterpret_cast<float*>(w + L.xa);
+    float* E = reinterpret_cast<float*>(w + 2 * L.xa);
+    float* Gk = reinterpret_cast<float*>(w + 2 * L.xa + L.e);
+    float* G1 = reinterpret_cast<float*>(w + 2 * L.xa + L.e + L.gk);
+    float* ones = reinterpret_cast<float*>(w + 2 * L.xa + L.e + L.gk + L.g1);
+    float* E1 = reinterpret_cast<float*>(w + 2 * L.xa + L.e + L.gk + L.g1 + L.ones);
+    const int kc = kc_of(g.K);
+    const double osc = 0.5 / (P.sigma_v * P.sigma_v);  // data term 1/(2 sv^2) ||y - A x||^2
+    if (obj_trace) CK(cudaMemsetAsync(obj_trace, 0, (size_t)(n_iter + 1) * sizeof(double), s), "mbir");
+    uint64_t nl = 0;
+    if (n_iter > 0) {  // data curvature A^T A 1 of one slice (the same for every slice and channel)
+        Geometry g1 = g;
+        g1.Nr = 1;
+        g1.K = 1;
+        CK(mbir_ones(ones, g.Nc, s), "mbir ones");
+        CK(mbir_project(g, h->t, ones, 1, 1, nullptr, 0, E1, 1, nullptr, 0.0, s), "mbir project");
+        CK(backproject(g1, h->t, E1, 1, 1, 0, 1, 0, G1, 0, 0, s), "mbir backprojection");
+        nl += 3;
+    }
+    CK(mbir_to_inner(X, g.K, Nx_of(g), Xa, s), "mbir");
+    nl += 1;
+    for (int it = 0; it < n_iter; ++it) {
+        double* o = obj_trace ? obj_trace + it : nullptr;
+        CK(mbir_project(g, h->t, Xa, g.Nr, g.K, V, 0, E, kc, o, osc, s), "mbir project");
+        CK(backproject(g, h->t, E, kc, g.K, 0, g.Nr, 0, Gk, 0, 0, s), "mbir backprojection");
+        CK(mbir_sqs(g, P, Xa, Gk, G1, Xb, it == n_iter - 1 ? X : nullptr, o, 1, h->t.status, s), "mbir update");
+        std::swap(Xa, Xb);
+        nl += 3;
+    }
+    if (obj_trace) {  // objective of the final iterate
+        CK(mbir_project(g, h->t, Xa, g.Nr, g.K, V, 0, E, kc, obj_trace + n_iter, osc, s), "mbir project");
+        CK(mbir_sqs(g, P, Xa, nullptr, nullptr, nullptr, nullptr, obj_trace + n_iter, 0, h->t.status, s), "mbir");
+        nl += 2;
+    }
+    h->launches += nl;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_project(hsnct_t h, const float* X, float* P, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_project");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "project: handle is NULL");
+    const Geometry& g = h->g;
+    if (!X || !P) return fail(HSNCT_E_ARG, "project: X or P is NULL");
+    if (!aligned(X, 4) || !aligned(P, 4)) return fail(HSNCT_E_ARG, "project: X, P must be 4-byte aligned");
+    const size_t need = mbir_layout(g).xa;
+    hsnct_status st;
+    if ((st = check_ws(ws, ws_bytes, need, "project"))) return st;
+    const Range rP = rng(P, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rX = rng(X, (size_t)Nx_of(g) * g.K * sizeof(float));
+    const Range rW = rng(ws, need);
+    if (overlap(rP, rX) || overlap(rW, rX) || overlap(rW, rP))
+        return fail(HSNCT_E_ARG, "project: X, P and workspace must not overlap");
+    DeviceGuard guard(h->device);
+    const cudaStream_t s = (cudaStream_t)stream;
+    float* Xi = static_cast<float*>(ws);
+    CK(mbir_to_inner(X, g.K, Nx_of(g), Xi, s), "project");
+    CK(mbir_project(g, h->t, Xi, g.Nr, g.K, nullptr, 1, P, g.K, nullptr, 0.0, s), "project");
+    h->launches += 2;
     return HSNCT_OK;
 }
 

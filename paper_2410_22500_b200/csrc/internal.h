@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 namespace hsnct {
 
@@ -58,6 +59,8 @@ struct DeviceTables {
     unsigned* status = nullptr; // device status word
     unsigned* counter = nullptr;// grid "last block" tickets (zero between launches)
     unsigned long long* nclamp = nullptr;  // negative Y entries clamped to 0 by the last decompose
+    int* mbir_groups = nullptr; // [mbir_ng][mbir_vb + 1] projector view groups (mbir.cu)
+    int mbir_ng = 0, mbir_vb = 0;
 };
 
 // ---------------------------------------------------------------- NMF (nmf.cu)
@@ -187,6 +190,31 @@ cudaError_t fmd_transform(const Geometry& g, const float* X, const int32_t* labe
 cudaError_t fmd_materials(const Geometry& g, const float* X, const float* T, int Nm, float* Xm, void* ws,
                           unsigned* status, cudaStream_t s);
 cudaError_t fmd_spectra(const Geometry& g, const float* D, const float* T, int Nm, float* Dm, cudaStream_t s);
+
+// ----------------------------------------------------------- MBIR (mbir.cu, NEXT-3)
+struct MbirPrm {
+    double sigma_v, sigma_x, p, q, T;
+};
+// Projector view groups: views split by orientation class (|cos| >= |sin|: 1, else 0), VB per
+// group; table[g*(vb+1)] = class, then VB views (-1 = empty slot).
+struct MbirGroups {
+    std::vector<int> table;
+    int ng = 0, vb = 0;
+};
+MbirGroups mbir_groups(const Geometry& g, const float* cs, const float* sn);
+int mbir_kp(int K);  // K rounded up to even: channels per voxel of the internal iterate Xi
+// X[k][n] -> Xi[n][KP]
+cudaError_t mbir_to_inner(const float* X, int K, int64_t Nx, float* Xi, cudaStream_t s);
+// Xi1[n][2] = (1, 0), n < Nc^2
+cudaError_t mbir_ones(float* Xi1, int Nc, cudaStream_t s);
+// A x of Nr slices of Xi (K channels, KP = mbir_kp(K) per voxel).  mode 0: E[r][v][c][Kc] = Y - A x
+// (Y [Np][K] nullable), osc * (sum of squares) added to *obj (nullable); mode 1: P[Np][K] = A x.
+cudaError_t mbir_project(const Geometry& g, const DeviceTables& t, const float* Xi, int Nr, int K, const float* Y,
+                         int mode, float* out, int Kc, double* obj, double osc, cudaStream_t s);
+// one SQS step Xc -> Xn (update = 1; Xout nullable: also channel-planar), or only the prior term
+// of the objective at Xc (update = 0); G = (pi/Nv) A^T e [K][Nx], G1 = (pi/Nv) A^T (-A 1) [Nc^2]
+cudaError_t mbir_sqs(const Geometry& g, const MbirPrm& prm, const float* Xc, const float* G, const float* G1,
+                     float* Xn, float* Xout, double* obj, int update, unsigned* status, cudaStream_t s);
 
 // ------------------------------------------------------- synthesis (synth.cu)
 cudaError_t synthesize(const Geometry& g, const float* X, const float* D, int s0, int ns, int b0,

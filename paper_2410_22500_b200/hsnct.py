@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HSNCT_LIB") or os.path.join(_HERE, "libhsnct.so")
 
 OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
-OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD = range(5)
+OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD, OP_MBIR, OP_PROJECT = range(7)
 MAX_SUB = 16
 
 # hsnct_window_fn: void (*)(void* user, int slice0, int n_slices, const float* xh)
@@ -40,6 +40,12 @@ class _Geom(ctypes.Structure):
                 ("n_sub", ctypes.c_int32), ("angles", ctypes.POINTER(ctypes.c_double))]
 
 
+class MbirParams(ctypes.Structure):
+    """hsnct_mbir_params: Eq. 5 noise scale sigma_v and QGGMRF (sigma_x, p, q, T)."""
+    _fields_ = [("sigma_v", ctypes.c_double), ("sigma_x", ctypes.c_double), ("p", ctypes.c_double),
+                ("q", ctypes.c_double), ("T", ctypes.c_double)]
+
+
 def lib():
     """Load libhsnct.so (fails loudly if it was not built)."""
     global _lib
@@ -59,6 +65,10 @@ def lib():
             L.hsnct_subspace_decompose.argtypes = [vp, vp, i64, vp, vp, i32, vp, vp, sz, vp]
             L.hsnct_subspace_decompose.restype = i32
             L.hsnct_fbp.argtypes = [vp, vp, vp, vp, sz, vp]
+            L.hsnct_mbir.argtypes = [vp, vp, vp, i32, ctypes.POINTER(MbirParams), vp, vp, sz, vp]
+            L.hsnct_mbir.restype = i32
+            L.hsnct_project.argtypes = [vp, vp, vp, vp, sz, vp]
+            L.hsnct_project.restype = i32
             L.hsnct_fbp.restype = i32
             L.hsnct_synthesize.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, i64, vp]
             L.hsnct_synthesize.restype = i32
@@ -249,6 +259,32 @@ class Hsnct:
         _check(lib().hsnct_fbp(self._h, _ptr(V), _ptr(X), _ptr(ws), ws.numel() * ws.element_size(),
                                _stream(stream, self.device)))
         return X
+
+    def mbir(self, V, X, n_iter, sigma_v, sigma_x, p=1.2, q=2.0, T=1.0, obj_trace=None, ws=None, stream=None):
+        """Eq. 5 MBIR of the K subspace sinograms (hsnct_mbir): X [K, N_r, N_c, N_c] holds x0 and
+        is overwritten with the n_iter-th SQS iterate; obj_trace (fp64 [n_iter + 1]) optional."""
+        self._dev(V, "V", (self.Np, self.K))
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        if obj_trace is not None and (obj_trace.dtype != torch.float64 or obj_trace.device != self.device
+                                      or obj_trace.numel() < n_iter + 1 or not obj_trace.is_contiguous()):
+            raise HsnctError(E_ARG, f"obj_trace must be a contiguous float64 tensor of >= {n_iter + 1} entries")
+        prm = MbirParams(float(sigma_v), float(sigma_x), float(p), float(q), float(T))
+        ws = self.workspace(OP_MBIR) if ws is None else ws
+        _check(lib().hsnct_mbir(self._h, _ptr(V), _ptr(X), int(n_iter), ctypes.byref(prm),
+                                _ptr(obj_trace) if obj_trace is not None else None, _ptr(ws),
+                                ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        return X
+
+    def project(self, X, P=None, ws=None, stream=None):
+        """Forward projection A X of Eq. 5 (hsnct_project) -> P [N_p, K] (the layout of V)."""
+        self._dev(X, "X", (self.K, self.Nr, self.Nc, self.Nc))
+        if P is None:
+            P = torch.empty((self.Np, self.K), dtype=torch.float32, device=self.device)
+        self._dev(P, "P", (self.Np, self.K))
+        ws = self.workspace(OP_PROJECT) if ws is None else ws
+        _check(lib().hsnct_project(self._h, _ptr(X), _ptr(P), _ptr(ws), ws.numel() * ws.element_size(),
+                                   _stream(stream, self.device)))
+        return P
 
     def synthesize(self, X, D, slice0=0, n_slices=None, bin0=0, n_bins=None, Xh=None, stream=None):
         """x^h window = x^s (D^s)^T (hsnct_synthesize) -> Xh [n_slices*N_c^2, n_bins]."""
