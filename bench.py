@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-dhr", action="store_true")
     ap.add_argument("--no-fmd", action="store_true")
+    ap.add_argument("--no-mbir", action="store_true")
+    ap.add_argument("--mbir-iters", type=int, default=10, help="SQS iterations of the MBIR extra (NEXT-3)")
     ap.add_argument("--shard", action="store_true",
                     help="N > 1: split the config's slices over the ranks (strong scaling; one NCCL "
                          "all-reduce of B, H and two scalars per NMF iteration, NEXT-4) instead of replicas")
@@ -278,7 +280,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
             pr["Y"], pr["V0"] = Y, V0
             torch.cuda.empty_cache()
         cfg = sd.reduced(cfg, r1 - r0)
-        args.no_dhr = args.no_fmd = args.no_e2e = args.no_cpu = True
+        args.no_dhr = args.no_fmd = args.no_e2e = args.no_cpu = args.no_mbir = True
     h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=local_rank)
     V = torch.empty_like(V0)
     D = torch.empty_like(D0)
@@ -456,6 +458,57 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                "note": "transform (Eq. 7) + per-voxel NNLS (Eq. 8) + spectra (Eq. 9), not in the metric"}
         del lab, Xm, Dm, T, wsf
 
+    # MBIR of the subspace sinograms (NEXT-3, Eq. 5; outside the timed step and the metric):
+    # hsnct_mbir from x0 = max(FBP, 0) of this step's V; per-iteration time from two call lengths,
+    # the projector timed alone through hsnct_project (the same kernel and launch shape)
+    mbir = None
+    if not args.no_mbir and rank == 0 and args.mbir_iters > 1:
+        nmb = args.mbir_iters
+        wsm = h.workspace(hm.OP_MBIR)
+        wsp = h.workspace(hm.OP_PROJECT)
+        X0 = X.clamp(min=0)
+        Xm = torch.empty_like(X0)
+        Pm = torch.empty_like(V)
+        # R26: sigma_v = 5% of the rms of V, sigma_x = 20% of the mean positive x0; svMBIR's
+        # QGGMRF defaults p = 1.2, q = 2, T = 1 (the cost does not depend on the values)
+        sv = 0.05 * float(V.double().pow(2).mean().sqrt())
+        sx = 0.2 * float(X0[X0 > 0].double().mean()) if bool((X0 > 0).any()) else 1.0
+        sx = sx if sx > 0 else 1.0
+
+        def t_mbir(n):
+            Xm.copy_(X0)
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            h.mbir(V, Xm, n, sv, sx, ws=wsm)
+            b.record(stream)
+            h.sync()
+            return a.elapsed_time(b) * 1e-3
+        t_mbir(1)
+        t1, tn = t_mbir(1), t_mbir(nmb)
+        per = (tn - t1) / (nmb - 1)
+        h.project(Xm, Pm, ws=wsp)
+        torch.cuda.synchronize()
+        a, b = ev(), ev()
+        a.record(stream)
+        h.project(Xm, Pm, ws=wsp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t_pr = a.elapsed_time(b) * 1e-3
+        K = cfg.K
+        kp = K + (K & 1)
+        # the projector's shared-memory reads: 3 taps of kp floats per (bin, line, view, slice)
+        pr_smem = 3.0 * 4 * kp * cfg.Nc * cfg.Nc * cfg.Nv * cfg.Nr
+        smem_pk = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e9
+        mbir = {"n_iter": nmb, "ms_per_iter": per * 1e3, "ms_total": tn * 1e3, "setup_ms": (t1 - per) * 1e3,
+                "voxels_x_iter_per_s": K * cfg.Nx / per, "sigma_v": sv, "sigma_x": sx, "p": 1.2, "q": 2.0, "T": 1.0,
+                "project_ms": t_pr * 1e3,
+                "project_roofline": {"bound": "smem", "achieved": pr_smem / t_pr / 1e9, "peak": smem_pk,
+                                     "unit": "GB/s", "frac": pr_smem / t_pr / 1e9 / smem_pk},
+                "note": "x0 = max(FBP, 0); one iteration = projector (e = y - A x) + backprojector (A^T e) + SQS "
+                        "update; not in the metric"}
+        del wsm, wsp, X0, Xm, Pm
+
     # end to end through the public API on page-locked HOST buffers (hsnct_fhr_stream): the
     # timed region holds, every step, the H2D copy of Y, V0, D0, the three stages, and the D2H
     # copy of ALL of x^h (window by window into a two-window host ring, overlapped with the
@@ -513,7 +566,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                 "data": "synthetic (seeded Bragg-edge ellipse phantom, Poisson counts, -log)",
                 "config": config_dict(gcfg, n_iter, world, shard),
                 "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "clocks": clk.summary()}
+                "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "mbir": mbir, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

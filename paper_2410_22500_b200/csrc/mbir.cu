@@ -66,16 +66,28 @@ __global__ void k_ones(float2* __restrict__ Xi, int64_t n) {
 // bins base + 32 m + l, m < CPT.  Per line L and bin c the pixels with |u - c| < 1 lie in
 // (pc - 1/|a|, pc + 1/|a|), pc the position where u = c, a the position's coefficient
 // (|a| >= 1/sqrt 2): at most three consecutive positions, from ceil(pc - 1/|a| - 1e-3).
+// Every staged line carries PPAD zero positions on both sides and p0 is clamped to
+// [-PPAD, Nc + PPAD - 3], so the three taps never leave the strip and need no bounds test
+// (a clamped p0 lies >= 1 position away from the bin: weight 0).
+// Strip layout: row class [line][PPAD + pos][KP] (a line = one contiguous image row);
+// column class [PPAD + pos][line][KP] (per image row, the strip's columns are contiguous), the
+// position pitch padded to an odd number of 8-byte words (bank spread of a warp's taps).
 // mode 0: out = E[r][v][c][Kc] = y - A x (y = Y[((v Nr + r) Nc + c) K + k], or -A x if Y is
-//         NULL), channels K..Kc-1 zero; the sum of e^2 is added to *obj (nullable).
+//         NULL), channels K..Kc-1 zero; osc * sum of e^2 is added to *obj (nullable).
 // mode 1: out = P[((v Nr + r) Nc + c) K + k] = (A x), the layout of V.
+constexpr int PPAD = 4;
+__host__ __device__ inline int col_pitch(int R, int KP) { return R * KP + (((R * KP / 2) & 1) ? 0 : 2); }
+__host__ __device__ inline int strip_floats(int R, int Nc, int KP) {
+    return max(R * (Nc + 2 * PPAD) * KP, (Nc + 2 * PPAD) * col_pitch(R, KP));
+}
+
 template <int KP, int CPT>
 __global__ void __launch_bounds__(PT, 1) k_project(const float* __restrict__ Xi, int Nr, int Nc, int Nv,
                                                    const int* __restrict__ groups, int VB, int R,
                                                    const float* __restrict__ cos_t, const float* __restrict__ sin_t,
                                                    const float* __restrict__ Y, int K, int mode,
                                                    float* __restrict__ out, int Kc, double* obj, double osc) {
-    extern __shared__ __align__(16) float xs[];  // [2][R][Nc][KP]
+    extern __shared__ __align__(16) float xs[];  // [2][strip_floats]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r = blockIdx.y;
     const int* grp = groups + blockIdx.x * (VB + 1);
@@ -94,20 +106,36 @@ __global__ void __launch_bounds__(PT, 1) k_project(const float* __restrict__ Xi,
         ra = fabsf(inv);
     }
     const float* Xr = Xi + (int64_t)r * Nc * Nc * KP;
-    const int lineF = Nc * KP;          // floats per staged line
+    const int SF = strip_floats(R, Nc, KP);
+    // element (line l, position p) of a strip at l * sL + (p + PPAD) * sP floats
+    const int sL = rowcls ? (Nc + 2 * PPAD) * KP : KP;
+    const int sP = rowcls ? KP : col_pitch(R, KP);
     const int nchk = (Nc + R - 1) / R;
 
-    // strip ck (lines ck*R .. ck*R+R-1) into buffer bf: 8-byte copies, zero beyond the image
+    // zero padding positions of both buffers (never written by the copies)
+    for (int t = tid; t < 2 * R * 2 * PPAD * (KP / 2); t += PT) {
+        const int e2 = t % (KP / 2), q = t / (KP / 2);
+        const int pp = q % (2 * PPAD), lq = q / (2 * PPAD), l = lq % R, bf = lq / R;
+        const int p = pp < PPAD ? pp - PPAD : Nc + pp - PPAD;
+        *reinterpret_cast<float2*>(xs + bf * SF + l * sL + (p + PPAD) * sP + 2 * e2) = make_float2(0.f, 0.f);
+    }
+
+    // strip ck (lines ck*R .. ck*R+nl-1) into buffer bf, 8-byte copies
     auto stage = [&](int ck, int bf) {
-        float* dst = xs + (size_t)bf * R * lineF;
-        const int n2 = R * lineF / 2;
-        for (int t = tid; t < n2; t += PT) {
-            const int l = t / (lineF / 2), rem = t - l * (lineF / 2);
-            const int p = rem / (KP / 2), ch = (rem - p * (KP / 2)) * 2;
-            const int L = ck * R + l;
-            const bool ok = L < Nc;
-            const int64_t src = rowcls ? ((int64_t)L * Nc + p) * KP + ch : ((int64_t)p * Nc + L) * KP + ch;
-            cp_async8(dst + (size_t)l * lineF + p * KP + ch, ok ? Xr + src : Xr, ok);
+        float* dst = xs + bf * SF;
+        const int L0 = ck * R, nl = min(R, Nc - L0);
+        if (rowcls) {
+            for (int l = 0; l < nl; ++l) {
+                const float* src = Xr + (int64_t)(L0 + l) * Nc * KP;
+                float* d = dst + l * sL + PPAD * KP;
+                for (int e = tid; e < Nc * KP / 2; e += PT) cp_async8(d + 2 * e, src + 2 * e, true);
+            }
+        } else {
+            for (int p = warp; p < Nc; p += PW) {
+                const float* src = Xr + ((int64_t)p * Nc + L0) * KP;
+                float* d = dst + (p + PPAD) * sP;
+                for (int e = lane; e < nl * KP / 2; e += 32) cp_async8(d + 2 * e, src + 2 * e, true);
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -129,28 +157,26 @@ __global__ void __launch_bounds__(PT, 1) k_project(const float* __restrict__ Xi,
         }
         __syncthreads();
         if (v >= 0) {
-            const float* strip = xs + (size_t)bf * R * lineF;
+            const float* strip = xs + bf * SF + PPAD * sP;
             const int nl = min(R, Nc - ck * R);
             for (int l = 0; l < nl; ++l) {
-                const float Lf = (float)(ck * R + l) - half;
-                const float t = fmaf(Lf, b, half);
-                const float* line = strip + (size_t)l * lineF;
+                const float t = fmaf((float)(ck * R + l) - half, b, half);
+                const float* line = strip + l * sL;
 #pragma unroll
                 for (int m = 0; m < CPT; ++m) {
                     const float c = (float)(cbase + 32 * m);
                     const float pc = fmaf(c - t, inv, half);
-                    const int p0 = (int)ceilf(pc - ra - 1e-3f);
+                    const int p0 = min(max((int)ceilf(pc - ra - 1e-3f), -PPAD), Nc + PPAD - 3);
+                    float u = fmaf((float)p0 - half, a, t) - c;  // u(p0) - c, then + a per tap
+                    const float* px = line + p0 * sP;
 #pragma unroll
                     for (int q3 = 0; q3 < 3; ++q3) {
-                        const int p = p0 + q3;
-                        const float u = fmaf((float)p - half, a, t);
-                        float w = fmaxf(0.f, 1.f - fabsf(u - c));
-                        const bool in = p >= 0 && p < Nc;
-                        w = in ? w : 0.f;
-                        const float* px = line + (in ? p : 0) * KP;
+                        const float w = fmaxf(0.f, 1.f - fabsf(u));
+                        u += a;
 #pragma unroll
                         for (int q = 0; q < KP / 2; ++q)
-                            acc[m][q] = ffma2(make_float2(w, w), *reinterpret_cast<const float2*>(px + 2 * q), acc[m][q]);
+                            acc[m][q] = ffma2(make_float2(w, w), *reinterpret_cast<const float2*>(px + q3 * sP + 2 * q),
+                                              acc[m][q]);
                     }
                 }
             }
@@ -334,13 +360,13 @@ MbirGroups mbir_groups(const Geometry& g, const float* cs, const float* sn) {
     return G;
 }
 
-static int strip_lines(int Nc, int KP) { return std::max(1, std::min(16, 24576 / (Nc * KP))); }
+static int strip_lines(int Nc, int KP) { return std::max(1, std::min(16, 24576 / ((Nc + 2 * PPAD) * KP))); }
 
 template <int KP, int CPT>
 static cudaError_t project_k(const Geometry& g, const DeviceTables& t, const float* Xi, int Nr, int K,
                              const float* Y, int mode, float* out, int Kc, double* obj, double osc, cudaStream_t s) {
     const int R = strip_lines(g.Nc, KP);
-    const size_t smem = (size_t)2 * R * g.Nc * KP * sizeof(float);
+    const size_t smem = (size_t)2 * strip_floats(R, g.Nc, KP) * sizeof(float);
     static SmemAttr attr;
     cudaError_t e = ensure_smem((const void*)k_project<KP, CPT>, (int)smem, attr);
     if (e != cudaSuccess) return e;
