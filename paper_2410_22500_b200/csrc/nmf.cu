@@ -592,6 +592,10 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.Nkp = (g.Nk + 3) & ~3;
     p.nbx = (g.Nk + 31) / 32;
     p.fused = nmf_fused_plan(g, num_sms, &p);
+    {  // HSNCT_NMF=twopass: the two-pass kernels (k_vstep + k_bpart + k_dred) on any shape
+        const char* nm = getenv("HSNCT_NMF");
+        if (nm && strcmp(nm, "twopass") == 0) p.fused = false;
+    }
     const char* np_env = getenv("HSNCT_NO_PERSIST");
     p.persist = p.fused && p.persist_fits && !(np_env && np_env[0] == '1');
     // tcgen05 row pass: HSNCT_NMF=tc / ffma forces the choice; by default the plan takes the
@@ -609,7 +613,7 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
             p.nby = num_sms * 8;
         }
     }
-    // two-pass fallback (K > 8 or very long spectra)
+    // two-pass fallback (very long spectra, or HSNCT_NMF=twopass)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
     const int64_t groups = (Np + VW * RPW - 1) / (VW * RPW);

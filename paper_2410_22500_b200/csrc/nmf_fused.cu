@@ -5,17 +5,30 @@
 
 namespace hsnct {
 
-// Ring slots per compute group: 3 when they fit the shared-memory budget, else 2.
+// Static shared memory of k_nmf_persist<K, ., nb, ngrp> (FusedShared + the D-update arrays),
+// with slack for alignment.
+static size_t persist_static_bytes(int K, int nb, int ngrp) {
+    const size_t KK = (size_t)K * K, GK = (size_t)RG * K, KP = (size_t)((K + 3) & ~3), nth = (size_t)ngrp * TG;
+    const size_t fs = 8 * ngrp * nb + 16 * ngrp + 4 * ngrp * nb + 4 * ngrp * 2 * GW * GK + 4 * ngrp * GW * RG * KP +
+                      4 * KK + 8 * ngrp * KK + 8 * ngrp + 4;
+    return fs + 24 * KK + 8 * nth + 8 * (nth / 32) + 8 * (size_t)K * 64 + 256;
+}
+
+// Ring slots per compute group: 3 when they fit the shared-memory budget, else 2.  K <= 8: the
+// measured 208 KB dynamic budget; K > 8 (larger static arrays): 227 KB less the static part
+// and the 1 KB the driver reserves per CTA.
 static int nbuf_for(int Nkp, int LP, int K, int ngrp) {
-    for (int nb = 3; nb >= 2; --nb)
-        if (fused_smem_bytes(Nkp, K, LP, nb, ngrp) <= 208 * 1024) return nb;
+    for (int nb = 3; nb >= 2; --nb) {
+        const size_t dyn = fused_smem_bytes(Nkp, K, LP, nb, ngrp);
+        const bool fits = K <= 8 ? dyn <= 208 * 1024 : dyn + persist_static_bytes(K, nb, ngrp) <= 226 * 1024;
+        if (fits) return nb;
+    }
     return 0;
 }
 
 bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
-    // K <= 8: the V update maps one lane per (tile row, component), RG * K <= 32 lanes; K = 9..12
-    // instantiations measured wrong (C6 round 2), so K > 8 runs the two-pass kernels
-    if (g.K > 8) return false;
+    // K = 9..16: the V update takes NE = ceil(RG K / 32) (tile row, component) elements per lane
+    if (g.K > 16) return false;
     const int Nkp = (g.Nk + 3) & ~3;
     const int pairs = (g.Nk + 1) / 2;
     const int LP = (pairs + TG - 1) / TG;
@@ -59,7 +72,7 @@ cudaError_t nmf_yplus_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w
     return cudaGetLastError();
 }
 
-#define HSNCT_K8(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8)
+#define HSNCT_K8(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
 
 cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D,
                              int it, unsigned* status, cudaStream_t s) {

@@ -211,6 +211,7 @@ struct DLayout {
 template <int K, int LP, int NBG, int NGRP>
 struct Pass {
     static constexpr int GK = RG * K;
+    static constexpr int NE = (GK + 31) / 32;  // (tile row, component) elements per lane in the V update
     static constexpr int KP = (K + 3) & ~3;
     static constexpr int KK = K * K;
     static constexpr int DS = 2 * TG * LP;
@@ -330,30 +331,34 @@ struct Pass {
         //      warp transpose-reduce, partials published in red[parity of the running count]
         // ---- V-update factor of the tile in slot `bb` (lanes < GK; run between publishing the
         //      row partials and waiting for the group's, so it fills the barrier wait)
-        auto vfactor = [&](int bb, int64_t r0t, int nvt, float& rfac, float& vome) {
+        auto vfactor = [&](int bb, int64_t r0t, int nvt, float (&rfac)[NE], float (&vome)[NE]) {
             const float* slot = ring + (size_t)(g * NBG + bb) * tf;
-            rfac = 0.f;
-            vome = 0.f;
-            if (lane < GK) {  // V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old V rows
-                const int r = lane / K, k = lane - (lane / K) * K;
-                float vg = 0.f;
-                if (nvt == RG) {  // warp-uniform: every tile but the ragged last one
-                    const float* vrow = slot + (size_t)RG * Nkp + r * K;
 #pragma unroll
-                    for (int j = 0; j < K; ++j) vg = fmaf(vrow[j], sh.Gs[j * K + k], vg);
-                    vome = vrow[k];
-                } else {
-                    const bool in = r < nvt;
+            for (int e = 0; e < NE; ++e) {
+                const int s = lane + 32 * e;
+                rfac[e] = 0.f;
+                vome[e] = 0.f;
+                if (s < GK) {  // V[r][k] / max(sum_j V[r][j] G[j][k], 1e-30) from the old V rows
+                    const int r = s / K, k = s - (s / K) * K;
+                    float vg = 0.f;
+                    if (nvt == RG) {  // warp-uniform: every tile but the ragged last one
+                        const float* vrow = slot + (size_t)RG * Nkp + r * K;
 #pragma unroll
-                    for (int j = 0; j < K; ++j) vg = fmaf(in ? V[(r0t + r) * K + j] : 0.f, sh.Gs[j * K + k], vg);
-                    vome = in ? V[(r0t + r) * K + k] : 0.f;
+                        for (int j = 0; j < K; ++j) vg = fmaf(vrow[j], sh.Gs[j * K + k], vg);
+                        vome[e] = vrow[k];
+                    } else {
+                        const bool in = r < nvt;
+#pragma unroll
+                        for (int j = 0; j < K; ++j) vg = fmaf(in ? V[(r0t + r) * K + j] : 0.f, sh.Gs[j * K + k], vg);
+                        vome[e] = in ? V[(r0t + r) * K + k] : 0.f;
+                    }
+                    rfac[e] = __fdividef(vome[e], fmaxf(vg, 1e-30f));  // 2 ulp, no slow path (vg >= 1e-30)
                 }
-                rfac = __fdividef(vome, fmaxf(vg, 1e-30f));  // 2 ulp, no slow path (vg >= 1e-30)
             }
         };
         // (WV: the V-update factor first, in the same lambda -- the three-group schedule, whose
         //  code generation is sensitive to this order)
-        auto phase1 = [&]<bool WV>(int bb, int64_t ncount, int64_t r0t, int nvt, float& rfac, float& vome) {
+        auto phase1 = [&]<bool WV>(int bb, int64_t ncount, int64_t r0t, int nvt, float (&rfac)[NE], float (&vome)[NE]) {
             if constexpr (WV) vfactor(bb, r0t, nvt, rfac, vome);
             const float* slot = ring + (size_t)(g * NBG + bb) * tf;
             const float* yb = slot + 2 * tl;
@@ -434,21 +439,24 @@ struct Pass {
         };
         // ---- V update of the tile (every warp redundantly, lane s -> (r, k)) once the group's
         //      partials are in; new V rows to this warp's Vn copy, V store, <V_new, A>, H
-        auto vupdate = [&](int64_t r0t, int nvt, int64_t ncount, float rfac, float vome) {
+        auto vupdate = [&](int64_t r0t, int nvt, int64_t ncount, const float (&rfac)[NE], const float (&vome)[NE]) {
             const int par = (int)(ncount & 1);
-            const int s = lane;
-            if (s < GK) {
-                float a = 0.f;
 #pragma unroll
-                for (int w = 0; w < GW; ++w) a += sh.red[g][par][w][s];
-                float vn = a * rfac;
-                if (s / K >= nvt) vn = 0.f;
-                sh.Vn[g][wg][s / K][s - (s / K) * K] = vn;
-                if (wg == VWARP && s / K < nvt) {
-                    if (first && !(isfinite(vome) && vome >= 0.f)) bad |= ST_INIT_BAD;
-                    if (!isfinite(vn)) bad |= ST_NUMERIC;
-                    V[r0t * K + s] = vn;
-                    vdotA += (double)vn * (double)a;
+            for (int e = 0; e < NE; ++e) {
+                const int s = lane + 32 * e;
+                if (s < GK) {
+                    float a = 0.f;
+#pragma unroll
+                    for (int w = 0; w < GW; ++w) a += sh.red[g][par][w][s];
+                    float vn = a * rfac[e];
+                    if (s / K >= nvt) vn = 0.f;
+                    sh.Vn[g][wg][s / K][s - (s / K) * K] = vn;
+                    if (wg == VWARP && s / K < nvt) {
+                        if (first && !(isfinite(vome[e]) && vome[e] >= 0.f)) bad |= ST_INIT_BAD;
+                        if (!isfinite(vn)) bad |= ST_NUMERIC;
+                        V[r0t * K + s] = vn;
+                        vdotA += (double)vn * (double)a;
+                    }
                 }
             }
             __syncwarp();
@@ -518,7 +526,7 @@ struct Pass {
                 const bool cur = m < cnt;
                 const int64_t n = n0 + m;
                 const int nv = cur ? (int)min((int64_t)RG, Np - r0) : 0;
-                float rfac = 0.f, vome = 0.f;
+                float rfac[NE] = {}, vome[NE] = {};
                 if (cur) {
                     mbar_wait_s(fullb + 8u * (unsigned)b, ph);
                     phase1.template operator()<false>(b, n, r0, nv, rfac, vome);
@@ -543,7 +551,7 @@ struct Pass {
                 const int64_t n = n0 + m;
                 const int nv = (int)min((int64_t)RG, Np - r0);
                 mbar_wait_s(fullb + 8u * (unsigned)b, ph);
-                float rfac, vome;
+                float rfac[NE], vome[NE];
                 if constexpr (true) {
                     // split barrier: publish the partials, compute the V-update factor while the
                     // group's other warps finish (C2: 49.4 -> 48.2 us per iteration; with three
@@ -1050,5 +1058,7 @@ cudaError_t persist_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w
                                                      float*, int, double*, unsigned*, unsigned*, cudaStream_t);
 HSNCT_FUSED_EXTERN(1) HSNCT_FUSED_EXTERN(2) HSNCT_FUSED_EXTERN(3) HSNCT_FUSED_EXTERN(4)
 HSNCT_FUSED_EXTERN(5) HSNCT_FUSED_EXTERN(6) HSNCT_FUSED_EXTERN(7) HSNCT_FUSED_EXTERN(8)
+HSNCT_FUSED_EXTERN(9) HSNCT_FUSED_EXTERN(10) HSNCT_FUSED_EXTERN(11) HSNCT_FUSED_EXTERN(12)
+HSNCT_FUSED_EXTERN(13) HSNCT_FUSED_EXTERN(14) HSNCT_FUSED_EXTERN(15) HSNCT_FUSED_EXTERN(16)
 
 }  // namespace hsnct

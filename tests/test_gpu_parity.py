@@ -108,6 +108,28 @@ def test_nmf_deterministic_and_resumable(H):
     assert rel(outs[3][0], outs[0][0]) < 1e-5 and rel(outs[3][1], outs[0][1]) < 1e-5
 
 
+@pytest.mark.parametrize("cfg,n_iter", [(sd.custom(idx=14, Nc=32, Nv=16, Nr=4, Nk=1200, K=9, M=3), 12),
+                                        (sd.custom(idx=15, Nc=24, Nv=11, Nr=2, Nk=203, K=16, M=5), 10),
+                                        (sd.custom(idx=16, Nc=20, Nv=13, Nk=203, K=5, M=4), 10)])
+def test_nmf_twopass_plan(monkeypatch, cfg, n_iter):
+    """HSNCT_NMF=twopass: the k_vstep + k_bpart + k_dred kernels (the fallback for shapes the
+    fused kernel cannot hold) against the oracle, K = 5, 9, 16."""
+    monkeypatch.setenv("HSNCT_NMF", "twopass")
+    from paper_2410_22500_b200 import Hsnct
+    pr = sd.make_problem(cfg)
+    h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
+    assert h.debug_plan().startswith("twopass"), h.debug_plan()
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    obj = torch.zeros(2 * n_iter, dtype=torch.float64, device=DEV)
+    h.subspace_decompose(padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4), V, D, n_iter, obj_trace=obj)
+    h.sync()
+    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter, objective=True)
+    assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
+    np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
+    h.close()
+
+
 @pytest.mark.parametrize("cfg,n_iter", [(sd.CONFIGS[1], 60),
                                         (sd.custom(idx=11, Nc=20, Nv=13, Nk=203, K=5, M=4), 25),
                                         (sd.custom(idx=12, Nc=32, Nv=16, Nr=4, Nk=1200, K=9, M=3), 15),
@@ -446,7 +468,8 @@ def test_argument_errors(H):
 @pytest.mark.parametrize("plan,cfg", [
     ("ffma", sd.CONFIGS[1]),
     ("tc", sd.CONFIGS[1]),
-    ("ffma", sd.custom(idx=71, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),      # K > 8: two-pass path
+    ("ffma", sd.custom(idx=71, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),      # K > 8 on the fused kernel
+    ("twopass", sd.custom(idx=73, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),   # the two-pass kernels
     ("ffma", sd.custom(idx=72, Nc=20, Nv=13, Nk=203, K=5, M=4)),            # ragged N_k (masked padding)
 ])
 def test_clamped_count_statistic(monkeypatch, plan, cfg):
