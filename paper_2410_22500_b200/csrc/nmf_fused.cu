@@ -35,6 +35,9 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     if (LP > lp_cap(g.K)) return false;
     // four groups (more tiles in flight) when the registers and two slots per group fit
     int ngrp = fits4(g.K, LP) && nbuf_for(Nkp, LP, g.K, 4) >= 2 ? 4 : 3;
+    // K > 8: two groups (8 warps, up to 255 registers): three spill 100-300 B of accumulators
+    // (C6, K = 9, LP = 5: 16.5 -> 15.5 ms per iteration)
+    if (g.K > 8) ngrp = 2;
     const char* ng = getenv("HSNCT_NGRP");
     if (ng && ng[0] == '3') ngrp = 3;
     const int nbuf = nbuf_for(Nkp, LP, g.K, ngrp);

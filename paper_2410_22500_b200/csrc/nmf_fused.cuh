@@ -1013,6 +1013,12 @@ inline cudaError_t disp_nb(const NmfPlan& p, F&& f) {
     constexpr int NG4 = fits4(K, LP) ? 4 : 3;
     if (p.ngrp == 4 && NG4 != 4) return cudaErrorInvalidValue;
     switch (p.nbuf * 10 + p.ngrp) {
+        case 22:
+            if constexpr (K > 8) return f.template operator()<K, LP, 2, 2>();
+            return cudaErrorInvalidValue;
+        case 32:
+            if constexpr (K > 8) return f.template operator()<K, LP, 3, 2>();
+            return cudaErrorInvalidValue;
         case 23: return f.template operator()<K, LP, 2, 3>();
         case 33: return f.template operator()<K, LP, 3, 3>();
         case 24: return f.template operator()<K, LP, 2, NG4>();
