@@ -92,6 +92,9 @@ def lib():
             L.oracle_nnls.argtypes = [_f64p, _int, _int, _f64p, _f64p]
             L.oracle_fmd_materials.restype = ctypes.c_int64
             L.oracle_fmd_materials.argtypes = [_f64p, _i64, _int, _f64p, _int, _f64p, _int]
+            L.oracle_counts_to_projections.restype = None
+            L.oracle_counts_to_projections.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, _i64, _i64,
+                                                       _i64, _f64p]
             L.oracle_fmd_spectra.restype = None
             L.oracle_fmd_spectra.argtypes = [_f64p, _i64, _int, _f64p, _int, _f64p]
             L.oracle_dhr.restype = _int
@@ -372,3 +375,17 @@ def mbir(V, Nv, Nr, Nc, X0, prm, n_iter, angles=None, nthreads=0):
                          int(nthreads)):
         raise ValueError("oracle_mbir: bad parameters")
     return X
+
+
+def counts_to_projections(y, y0, Nv, b=None):
+    """Eq. 2 + Appendix A (oracle.c): uint8 y [Np, Nk], y0 [Nr*Nc, Nk], b [Nv, Nk] or None -> p fp64."""
+    y = np.ascontiguousarray(y, dtype=np.uint8)
+    y0 = np.ascontiguousarray(y0, dtype=np.uint8)
+    Np, Nk = y.shape
+    NrNc = y0.shape[0]
+    assert Np == Nv * NrNc and y0.shape[1] == Nk
+    bb = None if b is None else _f64(b).reshape(Nv, Nk)
+    P = np.zeros((Np, Nk))
+    lib().oracle_counts_to_projections(y.ctypes.data, y0.ctypes.data, None if bb is None else bb.ctypes.data,
+                                       Nv, NrNc, Nk, _p64(P))
+    return P

@@ -744,3 +744,22 @@ int oracle_mbir(const double* V, int64_t Nv, int64_t Nr, int64_t Nc, int K, cons
     }
     return bad;
 }
+
+/* ------------------------------------------------------------------ counts -> projections (NEXT-1)
+ * Eq. 2 with the Appendix-A offset and the 1/2-count floor
+ * of reading R7:  p[v][r][c][k] = -log(max(y, 1/2) / max(y0, 1/2)) - b[v][k]
+ *                                = ln(max(y0, 1/2)) - ln(max(y, 1/2)) - b[v][k],  fp64.
+ * y: uint8 [Np][Nk], row p = (v Nr + r) Nc + c; y0: uint8 [Nr Nc][Nk] (open beam, one per (r, c));
+ * b: [Nv][Nk] (NULL = 0); P: [Np][Nk]. */
+void oracle_counts_to_projections(const uint8_t* y, const uint8_t* y0, const double* b, int64_t Nv, int64_t NrNc,
+                                  int64_t Nk, double* P) {
+    for (int64_t v = 0; v < Nv; ++v)
+        for (int64_t rc = 0; rc < NrNc; ++rc) {
+            const int64_t p = v * NrNc + rc;
+            for (int64_t k = 0; k < Nk; ++k) {
+                const double a = y0[rc * Nk + k] > 0 ? (double)y0[rc * Nk + k] : 0.5;
+                const double t = y[p * Nk + k] > 0 ? (double)y[p * Nk + k] : 0.5;
+                P[p * Nk + k] = log(a) - log(t) - (b ? b[v * Nk + k] : 0.0);
+            }
+        }
+}
