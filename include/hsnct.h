@@ -90,7 +90,8 @@ typedef enum {
     HSNCT_OP_FHR_HOST = 3,  /* hsnct_fhr_host                              */
     HSNCT_OP_FMD = 4,       /* hsnct_fmd_transform / hsnct_fmd_materials   */
     HSNCT_OP_MBIR = 5,      /* hsnct_mbir                                  */
-    HSNCT_OP_PROJECT = 6    /* hsnct_project                               */
+    HSNCT_OP_PROJECT = 6,   /* hsnct_project                               */
+    HSNCT_OP_DECOMPOSE_COUNTS = 7 /* hsnct_subspace_decompose_counts       */
 } hsnct_op;
 
 typedef struct {
@@ -132,6 +133,27 @@ size_t hsnct_workspace_bytes(hsnct_t h, int op);
 hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, float* V, float* D,
                                       int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
                                       void* stream);
+
+/* Counts-domain input (NEXT-1): Eq. 2 with the Appendix-A offset
+ * and the 1/2-count floor (R7),
+ *   Y[p][k] = fp32( (L[y0[rc][k]] - L[y[p][k]]) - b[v][k] ),  L[n] = ln(max(n, 1/2)) in fp64,
+ *   p = (v N_r + r) N_c + c, rc = r N_c + c:
+ * y uint8 [N_p][N_k] (transmitted counts, row p as for Y), y0 uint8 [N_r N_c][N_k] (the open
+ * beam, shared by every view), b fp32 [N_v][N_k] or NULL (= 0), all DEVICE memory, b 4-byte
+ * aligned.  The single fp64 -> fp32 rounding makes Y bit-identical to fp32 of the fp64 formula.
+ * hsnct_counts_to_projections writes Y [N_p][ld_y] (ld_y >= N_k; padding untouched; a
+ * non-finite b is a deferred E_DATA).
+ * hsnct_subspace_decompose_counts is hsnct_subspace_decompose on that Y, decoded inside the
+ * input preparation (1 byte of y per element instead of 4 of Y; y0 is read once per view and
+ * served from L2): V, D, the objective trace and the clamped count are bit-identical to
+ * hsnct_subspace_decompose on the materialised Y.  Workspace:
+ * hsnct_workspace_bytes(h, HSNCT_OP_DECOMPOSE_COUNTS) (device, 256-byte aligned); outputs
+ * and workspace must not overlap y, y0, b. */
+hsnct_status hsnct_counts_to_projections(hsnct_t h, const uint8_t* y, const uint8_t* y0, const float* b, float* Y,
+                                         int64_t ld_y, void* stream);
+hsnct_status hsnct_subspace_decompose_counts(hsnct_t h, const uint8_t* y, const uint8_t* y0, const float* b, float* V,
+                                             float* D, int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
+                                             void* stream);
 
 /* Sharded subspace extraction (NEXT-4): Eq. 4 on Y distributed over ranks by
  * rows (e.g. slice ranges: parallel-beam slices decouple, so a rank's rows are all views of its

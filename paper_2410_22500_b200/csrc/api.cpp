@@ -101,6 +101,12 @@ int64_t Nx_of(const Geometry& g) { return (int64_t)g.Nr * g.Nc * g.Nc; }
 int kc_of(int K) { return K <= 8 ? K : 16; }
 int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
 
+// hsnct_subspace_decompose_counts: the decompose workspace, plus (plans without a Y+ buffer: tc,
+// two-pass) the decoded Y [Np][Nkp]
+size_t counts_ws(const Geometry& g, const NmfPlan& p) {
+    return a256(nmf_ws_bytes(g, p)) + (p.fused ? 0 : a256((size_t)Np_of(g) * ((g.Nk + 3) & ~3) * sizeof(float)));
+}
+
 // hsnct_mbir workspace: two iterates Xi [Nx][KP], residual E [Np][Kc] (the backprojector's Q
 // layout), G = (pi/Nv) A^T E [K][Nx], and for A^T A 1: G1 [Nc^2], the ones image [Nc^2][2], E1 [Nv Nc]
 struct MbirLayout {
@@ -185,14 +191,14 @@ hsnct_status check_y(const Geometry& g, const float* Y, int64_t ld, const char* 
 
 // Enqueue decompose on device buffers (shared by the ABI call and fhr_host).
 hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, float* D, int n_iter,
-                           double* obj, void* ws, cudaStream_t s) {
+                           double* obj, void* ws, cudaStream_t s, const CountsIn* cin = nullptr) {
     if (n_iter == 0) return HSNCT_OK;
     NmfWs w = nmf_ws_carve(h->g, h->nmf, ws);
     w.nclamp = h->t.nclamp;
     CK(cudaMemsetAsync(h->t.nclamp, 0, sizeof(unsigned long long), s), "decompose stats");
     w.trace = h->trace;
     w.trace_iters = h->trace_iters;
-    CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s), "decompose init");
+    CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s, &h->t, cin), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
     if (h->nmf.persist) {
         const int nbx = (h->g.Nk + 31) / 32;
@@ -358,6 +364,10 @@ hsnct_status hsnct_create(const hsnct_geom* gp, int device, hsnct_t* out) {
     al((void**)&h->t.status, sizeof(unsigned));
     al((void**)&h->t.nclamp, sizeof(unsigned long long));
     al((void**)&h->t.counter, (size_t)(4 + (g.Nk + 31) / 32) * sizeof(unsigned));
+    std::vector<double> lt(256);
+    for (int n = 0; n < 256; ++n) lt[n] = std::log(n > 0 ? (double)n : 0.5);  // R7: ln(max(n, 1/2))
+    al((void**)&h->t.logtab, 256 * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(h->t.logtab, lt.data(), 256 * sizeof(double), cudaMemcpyHostToDevice);
     const MbirGroups mg = mbir_groups(g, cs.data(), sn.data());
     h->t.mbir_ng = mg.ng;
     h->t.mbir_vb = mg.vb;
@@ -401,6 +411,7 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.nclamp);
     cudaFree(h->t.counter);
     cudaFree(h->t.mbir_groups);
+    cudaFree(h->t.logtab);
     cudaFree(h->trace);
     for (cudaEvent_t e : h->fbp_ev)
         if (e) cudaEventDestroy(e);
@@ -423,6 +434,7 @@ size_t hsnct_workspace_bytes(hsnct_t h, int op) {
         case HSNCT_OP_FMD: return fmd_ws_bytes(h->g);
         case HSNCT_OP_MBIR: return mbir_layout(h->g).total;
         case HSNCT_OP_PROJECT: return mbir_layout(h->g).xa;
+        case HSNCT_OP_DECOMPOSE_COUNTS: return counts_ws(h->g, h->nmf);
         default: return 0;
     }
 }
@@ -454,6 +466,78 @@ hsnct_status hsnct_subspace_decompose(hsnct_t h, const float* Y, int64_t ld_y, f
         return fail(HSNCT_E_ARG, "decompose: Y, V, D, obj_trace and workspace must not overlap");
     DeviceGuard guard(h->device);
     return run_decompose(h, Y, ld_y, V, D, n_iter, obj_trace, ws, (cudaStream_t)stream);
+}
+
+hsnct_status check_counts(const Geometry& g, const uint8_t* y, const uint8_t* y0, const float* b, const char* op) {
+    if (!y || !y0) return fail(HSNCT_E_ARG, "%s: y or y0 is NULL", op);
+    if (b && !aligned(b, 4)) return fail(HSNCT_E_ARG, "%s: b must be 4-byte aligned", op);
+    (void)g;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_subspace_decompose_counts(hsnct_t h, const uint8_t* y, const uint8_t* y0, const float* b, float* V,
+                                             float* D, int n_iter, double* obj_trace, void* ws, size_t ws_bytes,
+                                             void* stream) {
+    Nvtx nvtx_("hsnct_subspace_decompose_counts");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "decompose_counts: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_counts(g, y, y0, b, "decompose_counts");
+    if (st) return st;
+    if (!V || !D) return fail(HSNCT_E_ARG, "decompose_counts: V or D is NULL");
+    if (!aligned(V, 16) || !aligned(D, 4))
+        return fail(HSNCT_E_ARG, "decompose_counts: V must be 16-byte aligned and D 4-byte aligned");
+    if (n_iter < 0) return fail(HSNCT_E_ARG, "decompose_counts: n_iter=%d < 0", n_iter);
+    if (obj_trace && !aligned(obj_trace, 8)) return fail(HSNCT_E_ARG, "decompose_counts: obj_trace misaligned");
+    const size_t need = counts_ws(g, h->nmf);
+    if ((st = check_ws(ws, ws_bytes, need, "decompose_counts"))) return st;
+    const Range ry = rng(y, (size_t)Np_of(g) * g.Nk), ry0 = rng(y0, (size_t)g.Nr * g.Nc * g.Nk);
+    const Range rb = rng(b, b ? (size_t)g.Nv * g.Nk * sizeof(float) : 0);
+    const Range rV = rng(V, (size_t)Np_of(g) * g.K * sizeof(float));
+    const Range rD = rng(D, (size_t)g.K * g.Nk * sizeof(float));
+    const Range rW = rng(ws, need);
+    const Range rO = rng(obj_trace, obj_trace ? (size_t)2 * n_iter * sizeof(double) : 0);
+    const Range outs[4] = {rV, rD, rW, rO}, ins[3] = {ry, ry0, rb};
+    for (int i = 0; i < 4; ++i) {
+        for (int j = i + 1; j < 4; ++j)
+            if (overlap(outs[i], outs[j])) return fail(HSNCT_E_ARG, "decompose_counts: V, D, obj_trace, ws overlap");
+        for (int j = 0; j < 3; ++j)
+            if (overlap(outs[i], ins[j]))
+                return fail(HSNCT_E_ARG, "decompose_counts: outputs and workspace must not overlap y, y0, b");
+    }
+    if (n_iter == 0) return HSNCT_OK;
+    DeviceGuard guard(h->device);
+    const cudaStream_t s = (cudaStream_t)stream;
+    const CountsIn cin{y, y0, b};
+    if (h->nmf.fused) return run_decompose(h, nullptr, 0, V, D, n_iter, obj_trace, ws, s, &cin);
+    // tc / two-pass plans read Y itself: decode it into the workspace tail first
+    float* Yd = reinterpret_cast<float*>(static_cast<char*>(ws) + a256(nmf_ws_bytes(g, h->nmf)));
+    const int Nkp = (g.Nk + 3) & ~3;
+    CK(counts_decode(g, h->t, cin, Yd, Nkp, 0, h->nmf.nby > 0 ? h->nmf.nby : g.num_sms * 8, nullptr, nullptr, s),
+       "decompose_counts decode");
+    h->launches += 1;
+    return run_decompose(h, Yd, Nkp, V, D, n_iter, obj_trace, ws, s);
+}
+
+hsnct_status hsnct_counts_to_projections(hsnct_t h, const uint8_t* y, const uint8_t* y0, const float* b, float* Y,
+                                         int64_t ld_y, void* stream) {
+    Nvtx nvtx_("hsnct_counts_to_projections");
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "counts_to_projections: handle is NULL");
+    const Geometry& g = h->g;
+    hsnct_status st = check_counts(g, y, y0, b, "counts_to_projections");
+    if (st) return st;
+    if (!Y || !aligned(Y, 4)) return fail(HSNCT_E_ARG, "counts_to_projections: Y is NULL or misaligned");
+    if (ld_y < g.Nk) return fail(HSNCT_E_ARG, "counts_to_projections: ld_y=%lld < N_k", (long long)ld_y);
+    const Range rY = rng(Y, ((size_t)Np_of(g) - 1) * ld_y * sizeof(float) + g.Nk * sizeof(float));
+    if (overlap(rY, rng(y, (size_t)Np_of(g) * g.Nk)) || overlap(rY, rng(y0, (size_t)g.Nr * g.Nc * g.Nk)) ||
+        overlap(rY, rng(b, b ? (size_t)g.Nv * g.Nk * sizeof(float) : 0)))
+        return fail(HSNCT_E_ARG, "counts_to_projections: Y must not overlap y, y0, b");
+    DeviceGuard guard(h->device);
+    CK(counts_decode(g, h->t, CountsIn{y, y0, b}, Y, ld_y, 0, g.num_sms * 8, nullptr, nullptr, (cudaStream_t)stream),
+       "counts_to_projections");
+    h->launches += 1;
+    return HSNCT_OK;
 }
 
 size_t hsnct_nmf_red_size(hsnct_t h) { return h ? nmf_red_size(h->g) : 0; }

@@ -60,6 +60,7 @@ struct DeviceTables {
     unsigned* counter = nullptr;// grid "last block" tickets (zero between launches)
     unsigned long long* nclamp = nullptr;  // negative Y entries clamped to 0 by the last decompose
     int* mbir_groups = nullptr; // [mbir_ng][mbir_vb + 1] projector view groups (mbir.cu)
+    double* logtab = nullptr;   // [256] ln(max(n, 1/2)), fp64 (counts.cu, R7)
     int mbir_ng = 0, mbir_vb = 0;
 };
 
@@ -135,8 +136,19 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p);
 NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws);
 // Enqueues the per-call preparation: G = D D^T for the initial D, and Y+ for the
 // fused path (nmf_init_launches launches).
+// counts-domain input (NEXT-1): uint8 y [Np][Nk], y0 [Nr Nc][Nk], offset b [Nv][Nk] (nullable)
+struct CountsIn {
+    const uint8_t* y;
+    const uint8_t* y0;
+    const float* b;
+};
+// mode 0: raw Y into out [Np][ld_out]; mode 1: Y+ into out [Np][Nkp] with the k_yplus partials
+// (nblk blocks: ypart[nblk], nclamp)
+cudaError_t counts_decode(const Geometry& g, const DeviceTables& t, const CountsIn& cin, float* out, int64_t ld_out,
+                          int mode, int nblk, double* ypart, unsigned long long* nclamp, cudaStream_t s);
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
-                            const float* D, unsigned* status, cudaStream_t s);
+                            const float* D, unsigned* status, cudaStream_t s, const DeviceTables* t = nullptr,
+                            const CountsIn* cin = nullptr);
 int nmf_init_launches(const NmfPlan& p);
 // Enqueues one Lee-Seung iteration (nmf_launches_per_iter launches).
 cudaError_t nmf_launch_iter(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y,

@@ -694,9 +694,14 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
 int nmf_init_launches(const NmfPlan& p) { return p.tc ? 3 : p.fused ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
-                            const float* D, unsigned* status, cudaStream_t s) {
+                            const float* D, unsigned* status, cudaStream_t s, const DeviceTables* t,
+                            const CountsIn* cin) {
+    if (cin && !p.fused) return cudaErrorInvalidValue;  // the caller decodes into a Y buffer instead
     if (p.tc) {
         cudaError_t e = nmf_tc_prepare(g, p, w, Y, ld_y, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.fused && cin) {  // Y+ decoded from the counts (NEXT-1), same partials as k_yplus
+        cudaError_t e = counts_decode(g, *t, *cin, w.Yp, p.Nkp, 1, p.nby, w.ypart, w.nclamp, s);
         if (e != cudaSuccess) return e;
     } else if (p.fused) {
         cudaError_t e = nmf_yplus_launch(g, p, w, Y, ld_y, status, s);

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HSNCT_LIB") or os.path.join(_HERE, "libhsnct.so")
 
 OK, E_ARG, E_DATA, E_NUMERIC, E_CUDA, E_NOMEM = range(6)
-OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD, OP_MBIR, OP_PROJECT = range(7)
+OP_DECOMPOSE, OP_FBP, OP_DHR, OP_FHR_HOST, OP_FMD, OP_MBIR, OP_PROJECT, OP_DECOMPOSE_COUNTS = range(8)
 MAX_SUB = 16
 
 # hsnct_window_fn: void (*)(void* user, int slice0, int n_slices, const float* xh)
@@ -68,6 +68,10 @@ def lib():
             L.hsnct_mbir.argtypes = [vp, vp, vp, i32, ctypes.POINTER(MbirParams), vp, vp, sz, vp]
             L.hsnct_mbir.restype = i32
             L.hsnct_project.argtypes = [vp, vp, vp, vp, sz, vp]
+            L.hsnct_counts_to_projections.argtypes = [vp, vp, vp, vp, vp, i64, vp]
+            L.hsnct_counts_to_projections.restype = i32
+            L.hsnct_subspace_decompose_counts.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, vp, sz, vp]
+            L.hsnct_subspace_decompose_counts.restype = i32
             L.hsnct_project.restype = i32
             L.hsnct_fbp.restype = i32
             L.hsnct_synthesize.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp, i64, vp]
@@ -259,6 +263,39 @@ class Hsnct:
         _check(lib().hsnct_fbp(self._h, _ptr(V), _ptr(X), _ptr(ws), ws.numel() * ws.element_size(),
                                _stream(stream, self.device)))
         return X
+
+    def _counts(self, y, y0, b):
+        for t, name, shape in ((y, "y", (self.Np, self.Nk)), (y0, "y0", (self.Nr * self.Nc, self.Nk))):
+            if not isinstance(t, torch.Tensor) or t.dtype != torch.uint8 or t.device != self.device \
+                    or tuple(t.shape) != shape or not t.is_contiguous():
+                raise HsnctError(E_ARG, f"{name} must be a contiguous uint8 tensor {shape} on {self.device}")
+        if b is not None:
+            self._dev(b, "b", (self.Nv, self.Nk))
+
+    def counts_to_projections(self, y, y0, b=None, Y=None, stream=None):
+        """Eq. 2 + Appendix A on uint8 counts (hsnct_counts_to_projections) -> Y [N_p, N_k]."""
+        self._counts(y, y0, b)
+        if Y is None:
+            Y = torch.empty((self.Np, self.Nk), dtype=torch.float32, device=self.device)
+        ld = self._rows(Y, "Y", self.Np, self.Nk)
+        _check(lib().hsnct_counts_to_projections(self._h, _ptr(y), _ptr(y0), _ptr(b) if b is not None else None,
+                                                 _ptr(Y), ld, _stream(stream, self.device)))
+        return Y
+
+    def subspace_decompose_counts(self, y, y0, V, D, n_iter, b=None, obj_trace=None, ws=None, stream=None):
+        """hsnct_subspace_decompose on Y decoded from uint8 counts (hsnct_subspace_decompose_counts)."""
+        self._counts(y, y0, b)
+        self._dev(V, "V", (self.Np, self.K))
+        self._dev(D, "D", (self.K, self.Nk))
+        if obj_trace is not None and (obj_trace.dtype != torch.float64 or obj_trace.device != self.device
+                                      or obj_trace.numel() < 2 * n_iter or not obj_trace.is_contiguous()):
+            raise HsnctError(E_ARG, "obj_trace must be a contiguous float64 device tensor of 2*n_iter")
+        ws = self.workspace(OP_DECOMPOSE_COUNTS) if ws is None else ws
+        _check(lib().hsnct_subspace_decompose_counts(self._h, _ptr(y), _ptr(y0), _ptr(b) if b is not None else None,
+                                                     _ptr(V), _ptr(D), int(n_iter),
+                                                     _ptr(obj_trace) if obj_trace is not None else None, _ptr(ws),
+                                                     ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        return V, D
 
     def mbir(self, V, X, n_iter, sigma_v, sigma_x, p=1.2, q=2.0, T=1.0, obj_trace=None, ws=None, stream=None):
         """Eq. 5 MBIR of the K subspace sinograms (hsnct_mbir): X [K, N_r, N_c, N_c] holds x0 and
