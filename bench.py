@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-dhr", action="store_true")
     ap.add_argument("--no-fmd", action="store_true")
     ap.add_argument("--no-mbir", action="store_true")
+    ap.add_argument("--no-counts", action="store_true")
     ap.add_argument("--mbir-iters", type=int, default=10, help="SQS iterations of the MBIR extra (NEXT-3)")
     ap.add_argument("--shard", action="store_true",
                     help="N > 1: split the config's slices over the ranks (strong scaling; one NCCL "
@@ -265,7 +266,8 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
         dist.init_process_group("nccl", device_id=dev)
     peaks = load_peaks()
 
-    pr = sd.make_problem(cfg, device=dev)
+    # uint8 counts y, y0 as well (NEXT-1 extra; Y is their Eq. 2 decode, bit for bit)
+    pr = sd.make_problem(cfg, device=dev, return_counts=not args.no_counts and not args.shard)
     Y, V0, D0 = pr["Y"], pr["V0"], pr["D0"]
     shard = args.shard  # at N = 1 the split iteration without a collective (a path check)
     gcfg = cfg  # the global workload (the metric counts its voxel*lambda)
@@ -280,7 +282,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
             pr["Y"], pr["V0"] = Y, V0
             torch.cuda.empty_cache()
         cfg = sd.reduced(cfg, r1 - r0)
-        args.no_dhr = args.no_fmd = args.no_e2e = args.no_cpu = args.no_mbir = True
+        args.no_dhr = args.no_fmd = args.no_e2e = args.no_cpu = args.no_mbir = args.no_counts = True
     h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=local_rank)
     V = torch.empty_like(V0)
     D = torch.empty_like(D0)
@@ -509,6 +511,37 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                         "update; not in the metric"}
         del wsm, wsp, X0, Xm, Pm
 
+    # counts-domain input (NEXT-1, outside the timed step): one-iteration decompositions from the
+    # fp32 Y and from the uint8 counts (the input preparation is the only difference; results are
+    # bit-identical), and the full decomposition from counts
+    counts = None
+    if not args.no_counts and rank == 0 and "y" in pr:
+        yc, y0c = pr["y"], pr["y0"]
+
+        def t_dec(fn, n):
+            V.copy_(V0)
+            D.copy_(D0)
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            fn(n)
+            b.record(stream)
+            h.sync()
+            return a.elapsed_time(b) * 1e-3
+        f_y = lambda n: h.subspace_decompose(Y, V, D, n, ws=ws_nmf)  # noqa: E731
+        f_c = lambda n: h.subspace_decompose_counts(yc, y0c, V, D, n, ws=ws_nmf)  # noqa: E731
+        t_dec(f_c, 1)
+        t1y, t1c = t_dec(f_y, 1), t_dec(f_c, 1)
+        tfull = t_dec(f_c, n_iter)
+        counts = {"decompose_1it_ms_fp32_input": t1y * 1e3, "decompose_1it_ms_counts_input": t1c * 1e3,
+                  "prep_saving_ms": (t1y - t1c) * 1e3, "decompose_ms_counts_input": tfull * 1e3,
+                  "input_bytes_fp32": 4 * cfg.Np * cfg.Nk, "input_bytes_counts": cfg.Np * cfg.Nk + cfg.Nr * cfg.Nc * cfg.Nk,
+                  "note": "hsnct_subspace_decompose_counts: Eq. 2 decoded inside the Y+ preparation; the "
+                          "iterations read the fp32 Y+ as before (bit-identical V, D)"}
+        del yc, y0c
+        pr.pop("y", None)
+        pr.pop("y0", None)
+
     # end to end through the public API on page-locked HOST buffers (hsnct_fhr_stream): the
     # timed region holds, every step, the H2D copy of Y, V0, D0, the three stages, and the D2H
     # copy of ALL of x^h (window by window into a two-window host ring, overlapped with the
@@ -566,7 +599,7 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                 "data": "synthetic (seeded Bragg-edge ellipse phantom, Poisson counts, -log)",
                 "config": config_dict(gcfg, n_iter, world, shard),
                 "roofline": roof, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "mbir": mbir, "clocks": clk.summary()}
+                "gpu_launches": launches, "gpu_dhr": dhr, "fmd": fmd, "mbir": mbir, "counts": counts, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
