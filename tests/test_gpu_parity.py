@@ -56,6 +56,11 @@ def padded(Y, ld, fill=float("nan")):
     (sd.custom(idx=25, Nc=32, Nv=16, Nr=4, Nk=1200, K=9, M=3), 20),
     (sd.custom(idx=26, Nc=24, Nv=11, Nr=2, Nk=600, K=12, M=5), 12),
     (sd.custom(idx=27, Nc=20, Nv=9, Nr=1, Nk=333, K=10, M=4), 12),
+    # few rows, long spectra: the persistent kernel's D-update slice would not fit,
+    # the plan takes the per-iteration launches
+    (sd.custom(idx=28, Nc=16, Nv=8, Nr=1, Nk=1600, K=6, M=3), 10),
+    (sd.custom(idx=29, Nc=8, Nv=2, Nr=1, Nk=2048, K=3, M=2), 10),
+    (sd.custom(idx=30, Nc=12, Nv=4, Nr=1, Nk=1200, K=12, M=2), 8),
 ])
 def test_nmf_parity(H, cfg, n_iter):
     pr = sd.make_problem(cfg)
