@@ -103,6 +103,11 @@ struct NmfPlan {
     TcRanges tc_rg;
     int tc_Nk16;     // Nk rounded up to 16
     int64_t tc_Npad; // Np rounded up to the 64-row tile
+    // mma.sync row pass (nmf_mma.cu), K <= 8: one launch per iteration + k_dred
+    bool mma;
+    int mma_NB;      // 16-bin blocks per row = ceil(Nk / 16)
+    int mma_NBW;     // blocks per warp (template instance >= ceil(NB / 8))
+    int64_t mma_Npad;// Np rounded up to the 16-row tile
     // two-pass fallback (nmf.cu)
     int nblk_v, nchunk, bthreads, nlam_blk;
     int64_t rows_per_chunk;
@@ -168,6 +173,16 @@ cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
                            unsigned* status, cudaStream_t s);
 cudaError_t nmf_tc_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                           unsigned* status, cudaStream_t s);
+// max(Y+), max row norm, ||Y+||^2 partials, non-finite check, clamped count (k_tc_stats; tc and
+// mma paths)
+cudaError_t nmf_tc_stats(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                         unsigned* status, cudaStream_t s);
+// mma.sync path: plan (mma_* fields, nblk_f, nby), input preparation, one row pass
+bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p);
+cudaError_t nmf_mma_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
+                            unsigned* status, cudaStream_t s);
+cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
+                           unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
 // sharded decomposition (NEXT-4): one row pass -> the rank's sums in red (fp64 [K*N_k + K*K + 2]);
 // the D update from the all-reduced sums (identical on every rank)

@@ -613,6 +613,18 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
             p.nby = num_sms * 8;
         }
     }
+    // mma.sync row pass (HSNCT_NMF=mma)
+    {
+        const char* nm = getenv("HSNCT_NMF");
+        const bool force_mma = nm && strcmp(nm, "mma") == 0;
+        NmfPlan q = p;
+        if (force_mma && !p.tc && nmf_mma_plan(g, num_sms, &q)) {
+            p = q;
+            p.mma = true;
+            p.fused = false;
+            p.persist = false;
+        }
+    }
     // two-pass fallback (very long spectra, or HSNCT_NMF=twopass)
     p.smem_v = (size_t)g.K * p.Nkp * sizeof(float);
     int occ = (int)std::max<size_t>(1, std::min<size_t>(4, (200u * 1024u) / std::max<size_t>(p.smem_v + 4096, 1)));
@@ -629,9 +641,9 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
     p.rows_per_chunk = (Np + p.nchunk - 1) / p.nchunk;
     p.nchunk = (int)((Np + p.rows_per_chunk - 1) / p.rows_per_chunk);
     if (p.nchunk < 1) p.nchunk = 1;
-    p.P = p.tc ? p.tc_ncl : p.fused ? p.PB : p.nchunk;
-    p.PH = p.tc ? TC_CLUSTER * p.tc_ncl : p.fused ? p.PB : p.nchunk;
-    p.nvp = p.tc ? TC_CLUSTER * p.tc_ncl : p.fused ? p.PB : p.nblk_v;
+    p.P = p.tc ? p.tc_ncl : p.mma ? p.nblk_f : p.fused ? p.PB : p.nchunk;
+    p.PH = p.tc ? TC_CLUSTER * p.tc_ncl : p.mma ? p.nblk_f : p.fused ? p.PB : p.nchunk;
+    p.nvp = p.tc ? TC_CLUSTER * p.tc_ncl : p.mma ? p.nblk_f : p.fused ? p.PB : p.nblk_v;
     return p;
 }
 
@@ -654,6 +666,11 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     }
     if (p.tc) {
         b += align256((size_t)p.tc_Npad * p.tc_Nk16 * 4);             // Yc: fp16 hi + lo per element
+        b += align256((size_t)p.nby * sizeof(double));                // ypart
+        b += align256(2 * sizeof(unsigned));                          // ymax, max row norm
+    }
+    if (p.mma) {
+        b += align256((size_t)p.mma_Npad * p.mma_NB * 16 * 4);        // Yc: fp16 hi + lo per element
         b += align256((size_t)p.nby * sizeof(double));                // ypart
         b += align256(2 * sizeof(unsigned));                          // ymax, max row norm
     }
@@ -688,10 +705,15 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
         w.ypart = (double*)take((size_t)p.nby * sizeof(double));
         w.ymax = (unsigned*)take(2 * sizeof(unsigned));
     }
+    if (p.mma) {
+        w.Yc = take((size_t)p.mma_Npad * p.mma_NB * 16 * 4);
+        w.ypart = (double*)take((size_t)p.nby * sizeof(double));
+        w.ymax = (unsigned*)take(2 * sizeof(unsigned));
+    }
     return w;
 }
 
-int nmf_init_launches(const NmfPlan& p) { return p.tc ? 3 : p.fused ? 2 : 1; }
+int nmf_init_launches(const NmfPlan& p) { return (p.tc || p.mma) ? 3 : p.fused ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s, const DeviceTables* t,
@@ -699,6 +721,9 @@ cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w,
     if (cin && !p.fused) return cudaErrorInvalidValue;  // the caller decodes into a Y buffer instead
     if (p.tc) {
         cudaError_t e = nmf_tc_prepare(g, p, w, Y, ld_y, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.mma) {
+        cudaError_t e = nmf_mma_prepare(g, p, w, Y, ld_y, status, s);
         if (e != cudaSuccess) return e;
     } else if (p.fused && cin) {  // Y+ decoded from the counts (NEXT-1), same partials as k_yplus
         cudaError_t e = counts_decode(g, *t, *cin, w.Yp, p.Nkp, 1, p.nby, w.ypart, w.nclamp, s);
@@ -729,6 +754,9 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
     if (p.tc) {
         cudaError_t e = nmf_tc_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
+    } else if (p.mma) {
+        cudaError_t e = nmf_mma_launch(g, p, w, V, D, it, status, s);
+        if (e != cudaSuccess) return e;
     } else if (p.fused) {
         cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
@@ -748,13 +776,13 @@ static cudaError_t iter_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, c
     }
     dim3 gd(p.nbx, DG2);
     k_dred<K><<<gd, 256, 0, s>>>(w.Bpart, w.Hpart, p.P, p.PH, g.Nk, p.Nkp, D, w.Gd, w.vpart, p.nvp,
-                                 w.ypart, (p.fused || p.tc) ? p.nby : 0, w.L2B,
+                                 w.ypart, (p.fused || p.tc || p.mma) ? p.nby : 0, w.L2B,
                                  w.L2H, w.dpart, w.Gpart, w.ysq, first ? 1 : 0, obj2, counter + 1,
                                  counter, status);
     return cudaGetLastError();
 }
 
-int nmf_launches_per_iter(const NmfPlan& p) { return (p.fused || p.tc) ? 2 : 3; }
+int nmf_launches_per_iter(const NmfPlan& p) { return (p.fused || p.tc || p.mma) ? 2 : 3; }
 
 // ------------------------------------------------------ sharded decomposition (NEXT-4)
 size_t nmf_red_size(const Geometry& g) { return (size_t)g.K * g.Nk + (size_t)g.K * g.K + 2; }
@@ -766,6 +794,9 @@ static cudaError_t shard_rowpass_k(const Geometry& g, const NmfPlan& p, const Nm
     const bool first = it == 0;
     if (p.tc) {
         cudaError_t e = nmf_tc_launch(g, p, w, V, D, it, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.mma) {
+        cudaError_t e = nmf_mma_launch(g, p, w, V, D, it, status, s);
         if (e != cudaSuccess) return e;
     } else if (p.fused) {
         cudaError_t e = nmf_fused_launch(g, p, w, V, D, it, status, s);
@@ -784,7 +815,7 @@ static cudaError_t shard_rowpass_k(const Geometry& g, const NmfPlan& p, const Nm
         dim3 gb(p.nchunk, p.nlam_blk);
         k_bpart<K><<<gb, p.bthreads, 0, s>>>(Y, ld, Np, g.Nk, p.Nkp, V, p.rows_per_chunk, w.Bpart, w.Hpart);
     }
-    const bool yp = p.fused || p.tc;
+    const bool yp = p.fused || p.tc || p.mma;
     k_red_local<K><<<(K * g.Nk + 255) / 256, 256, 0, s>>>(w.Bpart, p.P, g.Nk, p.Nkp, w.Hpart, p.PH, w.vpart, p.nvp,
                                                           yp ? w.ypart : nullptr, yp ? p.nby : 0, red);
     return cudaGetLastError();
@@ -834,6 +865,9 @@ std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
         snprintf(b, sizeof b, "tc k_nmf_tc<K=%d> cluster=%d grid=%d ring=%d+%dx%d-bin bins/CTA=%d..%d +k_dred", g.K,
                  TC_CLUSTER, TC_CLUSTER * p.tc_ncl, p.tc_R, p.tc_R2, p.tc_rg.W, p.tc_rg.L[TC_CLUSTER - 1],
                  p.tc_rg.L[0]);
+    else if (p.mma)
+        snprintf(b, sizeof b, "mma k_nmf_mma<K=%d,NBW=%d> grid=%d 16-row tiles, %d blocks/row +k_dred", g.K,
+                 p.mma_NBW, p.nblk_f, p.mma_NB);
     else if (p.persist)
         snprintf(b, sizeof b, "persist k_nmf_persist<K=%d,LP=%d,NBG=%d,NGRP=%d> grid=%d", g.K, p.LP, p.nbuf,
                  p.ngrp, p.nblk_f);
