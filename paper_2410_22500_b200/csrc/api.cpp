@@ -101,10 +101,10 @@ int64_t Nx_of(const Geometry& g) { return (int64_t)g.Nr * g.Nc * g.Nc; }
 int kc_of(int K) { return K <= 8 ? K : 16; }
 int dhr_kc(const Geometry& g) { return g.P <= 1024 ? 16 : 8; }
 
-// hsnct_subspace_decompose_counts: the decompose workspace, plus (plans without a Y+ buffer: tc,
+// hsnct_subspace_decompose_counts: the decompose workspace, plus (plans that read Y itself: tc,
 // two-pass) the decoded Y [Np][Nkp]
 size_t counts_ws(const Geometry& g, const NmfPlan& p) {
-    return a256(nmf_ws_bytes(g, p)) + (p.fused ? 0 : a256((size_t)Np_of(g) * ((g.Nk + 3) & ~3) * sizeof(float)));
+    return a256(nmf_ws_bytes(g, p)) + ((p.fused || p.mma) ? 0 : a256((size_t)Np_of(g) * ((g.Nk + 3) & ~3) * sizeof(float)));
 }
 
 // hsnct_mbir workspace: two iterates Xi [Nx][KP], residual E [Np][Kc] (the backprojector's Q
@@ -509,7 +509,7 @@ hsnct_status hsnct_subspace_decompose_counts(hsnct_t h, const uint8_t* y, const 
     DeviceGuard guard(h->device);
     const cudaStream_t s = (cudaStream_t)stream;
     const CountsIn cin{y, y0, b};
-    if (h->nmf.fused) return run_decompose(h, nullptr, 0, V, D, n_iter, obj_trace, ws, s, &cin);
+    if (h->nmf.fused || h->nmf.mma) return run_decompose(h, nullptr, 0, V, D, n_iter, obj_trace, ws, s, &cin);
     // tc / two-pass plans read Y itself: decode it into the workspace tail first
     float* Yd = reinterpret_cast<float*>(static_cast<char*>(ws) + a256(nmf_ws_bytes(g, h->nmf)));
     const int Nkp = (g.Nk + 3) & ~3;

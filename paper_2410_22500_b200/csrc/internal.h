@@ -81,7 +81,7 @@ struct NmfPlan {
     int nvp;         // number of per-CTA objective partials
     // fused single-pass path (nmf_fused.cu), K <= 8
     bool fused;
-    bool persist;    // run all iterations in one cooperative launch (fused path)
+    bool persist;    // run all iterations in one cooperative launch (fused or mma path)
     bool persist_fits;  // the persistent kernel's lambda slice fits its D-update buffers
     int LP;          // lambda pairs per thread
     int nbuf;        // ring slots per compute group
@@ -183,6 +183,12 @@ cudaError_t nmf_mma_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w,
                             unsigned* status, cudaStream_t s);
 cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                            unsigned* status, cudaStream_t s);
+// the mma input preparation from counts (NEXT-1): Eq. 2 decoded into the block layout
+cudaError_t nmf_mma_prepare_counts(const Geometry& g, const NmfPlan& p, const NmfWs& w, const DeviceTables& t,
+                                   const CountsIn& cin, unsigned* status, cudaStream_t s);
+// all n_iter iterations in one cooperative launch (mma path, persist_fits); bar = 1 zeroed word
+cudaError_t nmf_mma_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D,
+                                   int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s);
 int nmf_launches_per_iter(const NmfPlan& p);
 // sharded decomposition (NEXT-4): one row pass -> the rank's sums in red (fp64 [K*N_k + K*K + 2]);
 // the D update from the all-reduced sums (identical on every rank)

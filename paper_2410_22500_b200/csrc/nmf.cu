@@ -29,6 +29,12 @@ constexpr int BROWS = 32;      // V rows staged per column-pass sub-chunk
 // default plan: the FFMA row pass everywhere -- the tcgen05 pass measured 0.53 of HBM at
 // C3 / C5 against the persistent FFMA kernel's 0.72 (profiles/r02/tc/)
 constexpr int64_t TC_MIN_ROWS = INT64_MAX;
+// The mma.sync row pass (one launch per iteration + k_dred) against the persistent FFMA kernel,
+// per iteration (scripts/tc_perf.py, profiles/r02/mma/): C1 19.6 vs 12.7 us, C2 59.2 vs 46.8 us
+// (its fixed per-iteration cost dominates below ~25 tiles per SM), C3 1.83 vs 2.39 ms, C4 3.94 vs
+// 5.47 ms, C5 8.35 vs 11.03 ms.  The slice-reduced C3-C5 shapes of the parity tests (61-65K rows)
+// take the same kernel as the full ones.
+constexpr int64_t MMA_MIN_ROWS = 60000;
 
 // two independent fp32 FMAs in one packed instruction (fma.rn.f32x2): same rounding as FFMA
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
@@ -613,16 +619,19 @@ NmfPlan nmf_plan(const Geometry& g, int num_sms) {
             p.nby = num_sms * 8;
         }
     }
-    // mma.sync row pass (HSNCT_NMF=mma)
+    // mma.sync row pass (nmf_mma.cu): the default from MMA_MIN_ROWS rows (K <= 8, N_k <= 1664);
+    // HSNCT_NMF=mma forces it, =ffma / =twopass / =tc exclude it
     {
         const char* nm = getenv("HSNCT_NMF");
         const bool force_mma = nm && strcmp(nm, "mma") == 0;
+        const bool want = force_mma || (!nm && Np >= MMA_MIN_ROWS) || (nm && nm[0] == '\0' && Np >= MMA_MIN_ROWS);
         NmfPlan q = p;
-        if (force_mma && !p.tc && nmf_mma_plan(g, num_sms, &q)) {
+        if (want && !p.tc && (p.fused || force_mma) && nmf_mma_plan(g, num_sms, &q)) {
             p = q;
             p.mma = true;
             p.fused = false;
-            p.persist = false;
+            // all iterations in one cooperative launch unless HSNCT_NO_PERSIST=1
+            p.persist = p.persist_fits && !(np_env && np_env[0] == '1');
         }
     }
     // two-pass fallback (very long spectra, or HSNCT_NMF=twopass)
@@ -718,8 +727,11 @@ int nmf_init_launches(const NmfPlan& p) { return (p.tc || p.mma) ? 3 : p.fused ?
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s, const DeviceTables* t,
                             const CountsIn* cin) {
-    if (cin && !p.fused) return cudaErrorInvalidValue;  // the caller decodes into a Y buffer instead
-    if (p.tc) {
+    if (cin && !p.fused && !p.mma) return cudaErrorInvalidValue;  // the caller decodes into a Y buffer instead
+    if (p.mma && cin) {
+        cudaError_t e = nmf_mma_prepare_counts(g, p, w, *t, *cin, status, s);
+        if (e != cudaSuccess) return e;
+    } else if (p.tc) {
         cudaError_t e = nmf_tc_prepare(g, p, w, Y, ld_y, status, s);
         if (e != cudaSuccess) return e;
     } else if (p.mma) {
@@ -866,8 +878,8 @@ std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
                  TC_CLUSTER, TC_CLUSTER * p.tc_ncl, p.tc_R, p.tc_R2, p.tc_rg.W, p.tc_rg.L[TC_CLUSTER - 1],
                  p.tc_rg.L[0]);
     else if (p.mma)
-        snprintf(b, sizeof b, "mma k_nmf_mma<K=%d,NBW=%d> grid=%d 16-row tiles, %d blocks/row +k_dred", g.K,
-                 p.mma_NBW, p.nblk_f, p.mma_NB);
+        snprintf(b, sizeof b, "mma k_nmf_mma<K=%d,NBW=%d,PERSIST=%d> grid=%d 16-row tiles, %d blocks/row%s", g.K,
+                 p.mma_NBW, p.persist ? 1 : 0, p.nblk_f, p.mma_NB, p.persist ? "" : " +k_dred");
     else if (p.persist)
         snprintf(b, sizeof b, "persist k_nmf_persist<K=%d,LP=%d,NBG=%d,NGRP=%d> grid=%d", g.K, p.LP, p.nbuf,
                  p.ngrp, p.nblk_f);

@@ -90,6 +90,7 @@ cudaError_t nmf_fused_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w
 
 cudaError_t nmf_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int n_iter,
                                double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
+    if (p.mma) return nmf_mma_persist_launch(g, p, w, V, D, n_iter, obj, bar, status, s);
     switch (g.K) {
 #define M(KV) \
     case KV: return persist_launch_k<KV>(g, p, w, V, D, n_iter, obj, bar, status, s);

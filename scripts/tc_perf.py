@@ -39,18 +39,23 @@ def main():
         V, D = V0.clone(), D0.clone()
         h.subspace_decompose(Y, V, D, 2)  # warm-up (and workspace allocation)
         h.sync()
-        V, D = V0.clone(), D0.clone()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        e0.record()
-        h.subspace_decompose(Y, V, D, n_iter)
-        e1.record()
-        h.sync()
-        ms = e0.elapsed_time(e1)
+        def timed(n):
+            V, D = V0.clone(), D0.clone()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            h.subspace_decompose(Y, V, D, n)
+            e1.record()
+            h.sync()
+            return e0.elapsed_time(e1), V, D
+        ms1, _, _ = timed(1)
+        ms, V, D = timed(n_iter)
+        it_ms = (ms - ms1) / max(1, n_iter - 1)  # marginal cost of one iteration (no input prep)
         by = n_iter * (4.0 * cfg.Np * cfg.Nk + 8.0 * cfg.Np * cfg.K)
         gbs = by / (ms * 1e-3) / 1e9
-        print(f"C{ci} {h.debug_plan()}: {ms / n_iter:.3f} ms/iter (incl. input prep), {gbs:.0f} GB/s, "
-              f"frac {gbs / peak:.3f}", flush=True)
+        gbi = (4.0 * cfg.Np * cfg.Nk + 8.0 * cfg.Np * cfg.K) / (it_ms * 1e-3) / 1e9
+        print(f"C{ci} {h.debug_plan()}: {ms / n_iter:.3f} ms/iter incl. input prep (frac {gbs / peak:.3f}); "
+              f"per iteration {it_ms:.4f} ms (frac {gbi / peak:.3f}); 1-iteration call {ms1:.3f} ms", flush=True)
         res[plan] = (V.cpu(), D.cpu())
         h.close()
         del h

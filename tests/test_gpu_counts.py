@@ -62,6 +62,7 @@ def test_generator_counts_decode_bitwise():
     ("nopersist", sd.custom(idx=54, Nc=20, Nv=13, Nk=203, K=5, M=4, counts=30.0)),
     ("twopass", sd.custom(idx=55, Nc=20, Nv=13, Nk=203, K=5, M=4, counts=30.0)),
     ("tc", sd.CONFIGS[1]),
+    ("mma", sd.custom(idx=56, Nc=20, Nv=13, Nk=203, K=5, M=4, counts=30.0)),
 ])
 def test_decompose_counts_bitwise(monkeypatch, plan, cfg):
     if plan == "nopersist":

@@ -473,6 +473,8 @@ def test_argument_errors(H):
 @pytest.mark.parametrize("plan,cfg", [
     ("ffma", sd.CONFIGS[1]),
     ("tc", sd.CONFIGS[1]),
+    ("mma", sd.CONFIGS[1]),
+    ("mma", sd.custom(idx=74, Nc=20, Nv=13, Nk=203, K=5, M=4)),             # ragged N_k and N_p
     ("ffma", sd.custom(idx=71, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),      # K > 8 on the fused kernel
     ("twopass", sd.custom(idx=73, Nc=24, Nv=10, Nr=2, Nk=64, K=12, M=5)),   # the two-pass kernels
     ("ffma", sd.custom(idx=72, Nc=20, Nv=13, Nk=203, K=5, M=4)),            # ragged N_k (masked padding)

@@ -32,6 +32,7 @@ def rel(a, b):
 @pytest.mark.parametrize("plan,cfg,n_iter", [
     ("ffma", sd.custom(idx=81, Nc=24, Nv=10, Nr=4, Nk=200, K=4, M=3), 25),
     ("tc", sd.custom(idx=82, Nc=32, Nv=12, Nr=3, Nk=400, K=5, M=4), 20),
+    ("mma", sd.custom(idx=84, Nc=32, Nv=12, Nr=3, Nk=400, K=5, M=4), 20),
     ("ffma", sd.custom(idx=83, Nc=20, Nv=9, Nr=2, Nk=96, K=10, M=4), 15),   # K > 8: two-pass
 ])
 def test_sharded_one_rank_matches_decompose_and_oracle(monkeypatch, plan, cfg, n_iter):
