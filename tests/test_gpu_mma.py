@@ -56,6 +56,11 @@ CASES = [
     (sd.custom(idx=58, Nc=16, Nv=8, Nr=1, Nk=96, K=3, M=3), 12),
     (sd.custom(idx=59, Nc=13, Nv=7, Nr=1, Nk=40, K=2, M=2), 12),     # 3 blocks: warps without bins
     (sd.custom(idx=70, Nc=24, Nv=9, Nr=2, Nk=1664, K=6, M=5), 10),    # 13 blocks on every warp
+    # K = 9..16: two column blocks of 8 components (the paper's N_s = 9, Table I)
+    (sd.custom(idx=75, Nc=32, Nv=16, Nr=2, Nk=1200, K=9, M=3), 15),   # the C6 shape class
+    (sd.custom(idx=76, Nc=20, Nv=13, Nk=203, K=12, M=5), 12),         # ragged N_k and N_p
+    (sd.custom(idx=77, Nc=24, Nv=10, Nr=2, Nk=1280, K=16, M=6), 8),   # K = 16 (per-iteration launches)
+    (sd.custom(idx=78, Nc=16, Nv=9, Nr=1, Nk=64, K=10, M=4), 10),     # 4 blocks: warps without bins
 ]
 
 
