@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
     static_assert(K >= 1 && K <= 16, "two n8 column blocks at most");
     constexpr int NC = mma_nc(K);
     constexpr int KK = K * K;
-    constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [8 NC][8 NC]
+    constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [2 NC values][NC column blocks][32 lanes]
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[MW][MNS];
     __shared__ uint64_t vfull[MNV];
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
 #pragma unroll
                     for (int q = 0; q < (NC > 1 ? 4 : 2); ++q) {  // rows g (q < 2), g + 8 (q >= 2)
                         const float ir = pow2(-evs[q >> 1 < NC ? q >> 1 : 0]);
-                        double& hd = hsh[warp][(g + 8 * (q >> 1)) * (8 * NC) + 2 * t + (q & 1) + 8 * nb2];
+                        double& hd = hsh[warp][(q * NC + nb2) * 32 + lane];  // lane-major: conflict-free
                         hd += (double)(hc[q] * (ir * ivB[nb2][q & 1]));
                     }
                 }
@@ -492,7 +492,10 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
         if (tid < KK) {
             const int ka = tid / K, kb = tid - (tid / K) * K;
             double h = 0.0;
-            for (int w = 0; w < MW; ++w) h += hsh[w][ka * (8 * NC) + kb];
+            // H[ka][kb] is the sum of lane 4 (ka % 8) + (kb % 8) / 2's value q = 2 (ka / 8) + kb % 2,
+            // column block kb / 8
+            const int hi = ((2 * (ka >> 3) + (kb & 1)) * NC + (kb >> 3)) * 32 + 4 * (ka & 7) + ((kb & 7) >> 1);
+            for (int w = 0; w < MW; ++w) h += hsh[w][hi];
             A.Hpart[(int64_t)c * KK + tid] = h;
         }
         if (tid == 0) {
