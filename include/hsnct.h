@@ -320,6 +320,17 @@ hsnct_status hsnct_debug_plan(hsnct_t h, char* buf, size_t n);
 hsnct_status hsnct_debug_fbp_timing(hsnct_t h, int on);
 hsnct_status hsnct_debug_fbp_times(hsnct_t h, float* ms);
 
+/* Diagnostics: stage timing of hsnct_subspace_decompose / _counts (bench.py's NMF roofline, measured
+ * on the dominant kernel's own launches).  hsnct_debug_nmf_timing(h, 1) makes every later
+ * decompose record CUDA events (on the call's stream) around its input preparation (Y+ or counts
+ * into the row pass's layout, G = D0 D0^T) and around its iterations (the one persistent launch,
+ * or the per-iteration launches); hsnct_debug_nmf_timing(h, 0) stops it (synchronises the
+ * device).  hsnct_debug_nmf_times waits for the last timed call and writes ms[2] = {preparation,
+ * iterations} (HOST array, milliseconds); HSNCT_E_ARG when no timed call was made since timing
+ * was switched on. */
+hsnct_status hsnct_debug_nmf_timing(hsnct_t h, int on);
+hsnct_status hsnct_debug_nmf_times(hsnct_t h, float* ms);
+
 /* Static description of a status code; never NULL. */
 const char* hsnct_status_string(hsnct_status st);
 

@@ -33,6 +33,8 @@ struct hsnct_s {
     int trace_iters = 0;
     cudaEvent_t fbp_ev[3] = {nullptr, nullptr, nullptr};  // stage timing of hsnct_fbp (diagnostics)
     bool fbp_timed = false;                               // events of the last call are recorded
+    cudaEvent_t nmf_ev[3] = {nullptr, nullptr, nullptr};  // stage timing of decompose (diagnostics)
+    bool nmf_timed = false;
     // hsnct_fhr_stream: D2H copy stream and per-window-buffer events (created on first use)
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_syn[2] = {nullptr, nullptr}, ev_cpy[2] = {nullptr, nullptr};
@@ -198,14 +200,19 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
     CK(cudaMemsetAsync(h->t.nclamp, 0, sizeof(unsigned long long), s), "decompose stats");
     w.trace = h->trace;
     w.trace_iters = h->trace_iters;
+    const bool timed = h->nmf_ev[0] != nullptr;
+    if (timed) CK(cudaEventRecord(h->nmf_ev[0], s), "decompose timing");
     CK(nmf_launch_init(h->g, h->nmf, w, Y, ld, D, h->t.status, s, &h->t, cin), "decompose init");
     h->launches += nmf_init_launches(h->nmf);
+    if (timed) CK(cudaEventRecord(h->nmf_ev[1], s), "decompose timing");
+    h->nmf_timed = timed;
     if (h->nmf.persist) {
         const int nbx = (h->g.Nk + 31) / 32;
         cudaError_t e = nmf_persist_launch(h->g, h->nmf, w, V, D, n_iter, obj, h->t.counter + 1 + nbx + 1,
                                            h->t.status, s);
         if (e == cudaSuccess) {
             h->launches += 1;
+            if (timed) CK(cudaEventRecord(h->nmf_ev[2], s), "decompose timing");
             return HSNCT_OK;
         }
         // cooperative launch refused (e.g. SMs shared with other work): per-iteration launches
@@ -217,6 +224,7 @@ hsnct_status run_decompose(hsnct_t h, const float* Y, int64_t ld, float* V, floa
            "decompose iteration");
         h->launches += nmf_launches_per_iter(h->nmf);
     }
+    if (timed) CK(cudaEventRecord(h->nmf_ev[2], s), "decompose timing");
     return HSNCT_OK;
 }
 
@@ -414,6 +422,8 @@ void hsnct_destroy(hsnct_t h) {
     cudaFree(h->t.logtab);
     cudaFree(h->trace);
     for (cudaEvent_t e : h->fbp_ev)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : h->nmf_ev)
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i) {
         if (h->ev_syn[i]) cudaEventDestroy(h->ev_syn[i]);
@@ -1067,6 +1077,35 @@ hsnct_status hsnct_debug_fbp_times(hsnct_t h, float* ms) {
     CK(cudaEventSynchronize(h->fbp_ev[2]), "debug_fbp_times");
     CK(cudaEventElapsedTime(&ms[0], h->fbp_ev[0], h->fbp_ev[1]), "debug_fbp_times");
     CK(cudaEventElapsedTime(&ms[1], h->fbp_ev[1], h->fbp_ev[2]), "debug_fbp_times");
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_debug_nmf_timing(hsnct_t h, int on) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_nmf_timing: handle is NULL");
+    DeviceGuard guard(h->device);
+    if (on && !h->nmf_ev[0]) {
+        for (cudaEvent_t& e : h->nmf_ev) CK(cudaEventCreate(&e), "debug_nmf_timing");
+    } else if (!on && h->nmf_ev[0]) {
+        CK(cudaDeviceSynchronize(), "debug_nmf_timing");
+        for (cudaEvent_t& e : h->nmf_ev) {
+            cudaEventDestroy(e);
+            e = nullptr;
+        }
+    }
+    h->nmf_timed = false;
+    return HSNCT_OK;
+}
+
+hsnct_status hsnct_debug_nmf_times(hsnct_t h, float* ms) {
+    g_last_error.clear();
+    if (!h) return fail(HSNCT_E_ARG, "debug_nmf_times: handle is NULL");
+    if (!ms) return fail(HSNCT_E_ARG, "debug_nmf_times: ms is NULL");
+    if (!h->nmf_timed) return fail(HSNCT_E_ARG, "debug_nmf_times: no timed decompose call");
+    DeviceGuard guard(h->device);
+    CK(cudaEventSynchronize(h->nmf_ev[2]), "debug_nmf_times");
+    CK(cudaEventElapsedTime(&ms[0], h->nmf_ev[0], h->nmf_ev[1]), "debug_nmf_times");
+    CK(cudaEventElapsedTime(&ms[1], h->nmf_ev[1], h->nmf_ev[2]), "debug_nmf_times");
     return HSNCT_OK;
 }
 

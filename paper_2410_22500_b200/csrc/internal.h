@@ -128,6 +128,7 @@ struct NmfWs {
     unsigned long long* nclamp = nullptr;  // clamped-entry counter (handle-owned, zeroed per call)
     void* Yc;        // [Npad*Nk16] Y+ as fp16 hi/lo pairs in the tcgen05 layout (tc path)
     unsigned* ymax;  // bits of max(Y+) (tc path)
+    int* texp;       // [ntiles] per-tile Y+ scale exponents (mma path)
     // diagnostics (hsnct_debug_trace): per-iteration, per-CTA %globaltimer stamps
     uint64_t* trace = nullptr;  // [trace_iters][nCTA][TRACE_SLOTS] or null
     int trace_iters = 0;

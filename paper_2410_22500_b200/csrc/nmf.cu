@@ -681,7 +681,7 @@ size_t nmf_ws_bytes(const Geometry& g, const NmfPlan& p) {
     if (p.mma) {
         b += align256((size_t)p.mma_Npad * p.mma_NB * 16 * 4);        // Yc: fp16 hi + lo per element
         b += align256((size_t)p.nby * sizeof(double));                // ypart
-        b += align256(2 * sizeof(unsigned));                          // ymax, max row norm
+        b += align256((size_t)(p.mma_Npad / 16) * sizeof(int));      // texp: per-tile scale exponents
     }
     return b;
 }
@@ -717,12 +717,12 @@ NmfWs nmf_ws_carve(const Geometry& g, const NmfPlan& p, void* ws) {
     if (p.mma) {
         w.Yc = take((size_t)p.mma_Npad * p.mma_NB * 16 * 4);
         w.ypart = (double*)take((size_t)p.nby * sizeof(double));
-        w.ymax = (unsigned*)take(2 * sizeof(unsigned));
+        w.texp = (int*)take((size_t)(p.mma_Npad / 16) * sizeof(int));
     }
     return w;
 }
 
-int nmf_init_launches(const NmfPlan& p) { return (p.tc || p.mma) ? 3 : p.fused ? 2 : 1; }
+int nmf_init_launches(const NmfPlan& p) { return p.tc ? 3 : (p.fused || p.mma) ? 2 : 1; }
 
 cudaError_t nmf_launch_init(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             const float* D, unsigned* status, cudaStream_t s, const DeviceTables* t,

@@ -5,155 +5,151 @@
 namespace hsnct {
 namespace {
 
-// Y+ (clamped, scaled by sigma_Y) split into fp16 hi/lo in the block layout above.  Item
-// (tile, block, core matrix q, row rr), rr fastest: 32 consecutive threads write one block's
-// hi and lo halves (512 contiguous bytes each); each reads 8 bins of one row.
-__global__ void __launch_bounds__(256) k_mma_convert(const float* __restrict__ Y, int64_t ld, int64_t Np, int Nk,
-                                                     int NB, int64_t ntiles, const unsigned* __restrict__ ymax,
-                                                     uint8_t* __restrict__ Yc) {
-    const float sy = pow2(mexp(__uint_as_float(*ymax)));
-    const int64_t n = ntiles * NB * 32;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int rr = (int)(i & 7), q = (int)((i >> 3) & 3);
-        const int64_t u = i >> 5;
-        const int j = (int)(u % NB);
-        const int64_t tt = u / NB;
-        const int64_t r = tt * MR + (q & 1) * 8 + rr;
-        const int l = 16 * j + (q >> 1) * 8;
-        float v[8];
+// ---- input preparation: Y+ (or Eq. 2 decoded from counts) into the block layout, one pass.
+// Block b takes tiles b, b + grid, ...: per tile a first sweep over its items (tile row, 8 bins)
+// for max Y+, ||Y+||^2, the non-finite check and the clamped count; the tile's scale exponent
+// (sigma_Y = 2^e, 2^e max < 2^14) to texp; a second sweep (L2-hot re-read) splits Y+ sigma_Y into
+// fp16 hi/lo blocks.  Item (block j, core matrix q, row rr), rr fastest: 32 consecutive threads
+// write one block's hi and lo halves (512 contiguous bytes each).  ||Y+||^2 partials per CUDA
+// block in a fixed order (deterministic).
+struct YSrc {  // fp32 Y [Np][ld]
+    const float* Y;
+    int64_t ld;
+    __device__ void stage(double*) const {}
+    __device__ void tile(int64_t) {}
+    template <bool LAST>
+    __device__ __forceinline__ void load8(int64_t r, int ri, int l, int64_t Np, int Nk, float (&v)[8]) const {
+        (void)ri;
         if (r < Np && l + 8 <= Nk) {
             const float4* y = reinterpret_cast<const float4*>(Y + r * ld + l);
-            const float4 a = __ldg(y), b = __ldg(y + 1);
+            const float4 a = LAST ? __ldcs(y) : __ldg(y), b = LAST ? __ldcs(y + 1) : __ldg(y + 1);
             v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
             v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
         } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e) v[e] = (r < Np && l + e < Nk) ? Y[r * ld + l + e] : 0.f;
         }
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            hw[e] = split2(fmaxf(v[2 * e], 0.f) * sy, fmaxf(v[2 * e + 1], 0.f) * sy, lw[e]);
-        uint8_t* dst = Yc + (size_t)u * BLK + q * 128 + rr * 16;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(dst + 512) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
     }
-}
-
-// ---- counts-domain input (NEXT-1): Eq. 2 with the Appendix-A offset decoded straight into the
-// block layout, Y = fp32((L[y0] - L[y]) - b) with the fp64 table L[n] = ln max(n, 1/2)
-// (counts.cu, R7): the same per-element value as hsnct_counts_to_projections, and the
-// two kernels below have the loop structure of k_tc_stats / k_mma_convert, so the decomposition
-// from counts is bit-identical to the one from the materialised Y.
-struct CountsSrc {
+};
+// uint8 counts: Y = fp32((L[y0] - L[y]) - b), L[n] = ln max(n, 1/2) in fp64 (counts.cu, DESIGN.md
+// R7): the same per-element value as hsnct_counts_to_projections, so the decomposition from
+// counts is bit-identical to the one from the materialised Y.
+struct CSrc {
     const uint8_t* y;    // [Np][Nk]
     const uint8_t* y0;   // [Nr Nc][Nk]
     const float* b;      // [Nv][Nk] or null
-    const double* L;     // [256] (device table)
+    const double* Lg;    // [256] (device table)
     int64_t NrNc;
-    int Nk;
-};
-struct CountsRow {  // the rows of y, y0 and b that row p of Y decodes from
-    const uint8_t* y;
-    const uint8_t* y0;
-    const float* b;
-};
-__device__ __forceinline__ CountsRow counts_row(const CountsSrc& C, int64_t p) {
-    const int64_t v = p / C.NrNc, rc = p - v * C.NrNc;
-    return {C.y + p * C.Nk, C.y0 + rc * C.Nk, C.b ? C.b + v * C.Nk : nullptr};
-}
-__device__ __forceinline__ float decode1(const CountsRow& R, const double* Ls, int l) {
-    double d = Ls[R.y0[l]] - Ls[R.y[l]];
-    if (R.b) d -= (double)R.b[l];
-    return (float)d;
-}
-
-// k_tc_stats (nmf_tc.cu) on decoded counts: max Y+ (bits), ||Y+||^2 per-block partials (same
-// per-row order), non-finite check (b), clamped count.  One warp per row.
-__global__ void __launch_bounds__(256) k_mma_counts_stats(CountsSrc C, int64_t Np, unsigned* __restrict__ ymax,
-                                                          double* __restrict__ ypart, unsigned* __restrict__ status,
-                                                          unsigned long long* __restrict__ nclamp) {
-    __shared__ double Ls[256];
-    __shared__ double red[8];
-    __shared__ unsigned mred[8], cred[8];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) Ls[i] = C.L[i];
-    __syncthreads();
-    unsigned ncl = 0;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int nq = (C.Nk + 3) >> 2;
-    double s = 0.0;
-    unsigned m = 0, bad = 0;
-    for (int64_t r = (int64_t)blockIdx.x * 8 + w; r < Np; r += (int64_t)gridDim.x * 8) {
-        const CountsRow R = counts_row(C, r);
-        float ps = 0.f;
-        for (int q = lane; q < nq; q += 32) {
-            const int l = 4 * q;
+    const double* L;     // the table in shared memory (stage)
+    int64_t v0, rc0;     // view and (r, c) index of the current tile's first row
+    __device__ void stage(double* Ls) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) Ls[i] = Lg[i];
+        L = Ls;
+    }
+    __device__ void tile(int64_t t) {
+        const int64_t r0 = t * 16;
+        v0 = r0 / NrNc;
+        rc0 = r0 - v0 * NrNc;
+    }
+    template <bool LAST>
+    __device__ __forceinline__ void load8(int64_t r, int ri, int l, int64_t Np, int Nk, float (&v)[8]) const {
+        int64_t rc = rc0 + ri, vv = v0;
+        if (rc >= NrNc) {  // the tile crosses into the next view
+            rc -= NrNc;
+            ++vv;
+        }
+        const uint8_t* yr = y + r * Nk;
+        const uint8_t* y0r = y0 + rc * Nk;
+        const float* br = b ? b + vv * Nk : nullptr;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float vj = l + j < C.Nk ? decode1(R, Ls, l + j) : 0.f;
-                if (!isfinite(vj)) bad = ST_Y_NONFINITE;
-                ncl += vj < 0.f;
-                const float yp = fmaxf(vj, 0.f);
-                m = max(m, __float_as_uint(yp));
+        for (int e = 0; e < 8; ++e) {
+            float f = 0.f;
+            if (r < Np && l + e < Nk) {
+                double d = L[y0r[l + e]] - L[yr[l + e]];
+                if (br) d -= (double)br[l + e];
+                f = (float)d;
+            }
+            v[e] = f;
+        }
+    }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(256) k_mma_prep(Src src, int64_t Np, int Nk, int NB, int64_t ntiles,
+                                                  uint8_t* __restrict__ Yc, int* __restrict__ texp,
+                                                  double* __restrict__ ypart, unsigned* __restrict__ status,
+                                                  unsigned long long* __restrict__ nclamp) {
+    __shared__ double Ls[256];
+    __shared__ float redm[8];
+    __shared__ double reds[8];
+    __shared__ unsigned redc[8];
+    src.stage(Ls);
+    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int nit = NB * 32;
+    double s = 0.0;
+    unsigned ncl = 0, bad = 0;
+    for (int64_t tt = blockIdx.x; tt < ntiles; tt += gridDim.x) {
+        src.tile(tt);
+        float m = 0.f, ps = 0.f;
+        for (int i = tid; i < nit; i += 256) {
+            const int rr = i & 7, q = (i >> 3) & 3, j = i >> 5;
+            const int ri = (q & 1) * 8 + rr;
+            float v[8];
+            src.template load8<false>(tt * MR + ri, ri, 16 * j + (q >> 1) * 8, Np, Nk, v);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (!isfinite(v[e])) bad = ST_Y_NONFINITE;
+                ncl += v[e] < 0.f;
+                const float yp = fmaxf(v[e], 0.f);
+                m = fmaxf(m, yp);
                 ps = fmaf(yp, yp, ps);
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
         s += (double)ps;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) redm[w] = m;
+        __syncthreads();
+        float tm = redm[0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) tm = fmaxf(tm, redm[u]);
+        const int e = mexp(tm);
+        const float sy = pow2(e);
+        if (tid == 0) texp[tt] = e;
+        for (int i = tid; i < nit; i += 256) {
+            const int rr = i & 7, q = (i >> 3) & 3, j = i >> 5;
+            const int ri = (q & 1) * 8 + rr;
+            float v[8];
+            src.template load8<true>(tt * MR + ri, ri, 16 * j + (q >> 1) * 8, Np, Nk, v);
+            uint32_t hw[4], lw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                hw[u] = split2(fmaxf(v[2 * u], 0.f) * sy, fmaxf(v[2 * u + 1], 0.f) * sy, lw[u]);
+            uint8_t* dst = Yc + ((size_t)tt * NB + j) * BLK + q * 128 + rr * 16;
+            *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+            *reinterpret_cast<uint4*>(dst + 512) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+        __syncthreads();  // redm is reused by the next tile
     }
-    m = __reduce_max_sync(0xffffffffu, m);
-    bad = __reduce_or_sync(0xffffffffu, bad);
+    s = warp_sum_d(s);
     ncl = __reduce_add_sync(0xffffffffu, ncl);
-    if (lane == 0) {  // (s is the same in every lane: the row sums were reduced over the warp)
-        red[w] = s;
-        mred[w] = m;
-        cred[w] = ncl;
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        reds[w] = s;
+        redc[w] = ncl;
         if (bad) atomicOr(status, bad);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double tt = 0.0;
-        unsigned mm = 0;
-        unsigned long long cc = 0;
-        for (int j = 0; j < 8; ++j) {
-            tt += red[j];
-            mm = max(mm, mred[j]);
-            cc += cred[j];
+    if (tid == 0) {
+        double t = 0.0;
+        unsigned long long c = 0;
+        for (int u = 0; u < 8; ++u) {
+            t += reds[u];
+            c += redc[u];
         }
-        ypart[blockIdx.x] = tt;
-        if (cc) atomicAdd(nclamp, cc);
-        if (mm) atomicMax(ymax, mm);
-    }
-}
-
-// k_mma_convert on decoded counts
-__global__ void __launch_bounds__(256) k_mma_counts_convert(CountsSrc C, int64_t Np, int NB, int64_t ntiles,
-                                                            const unsigned* __restrict__ ymax,
-                                                            uint8_t* __restrict__ Yc) {
-    __shared__ double Ls[256];
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) Ls[i] = C.L[i];
-    __syncthreads();
-    const float sy = pow2(mexp(__uint_as_float(*ymax)));
-    const int64_t n = ntiles * NB * 32;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int rr = (int)(i & 7), q = (int)((i >> 3) & 3);
-        const int64_t u = i >> 5;
-        const int j = (int)(u % NB);
-        const int64_t tt = u / NB;
-        const int64_t r = tt * MR + (q & 1) * 8 + rr;
-        const int l = 16 * j + (q >> 1) * 8;
-        float v[8];
-        const CountsRow R = counts_row(C, r < Np ? r : 0);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = (r < Np && l + e < C.Nk) ? decode1(R, Ls, l + e) : 0.f;
-        uint32_t hw[4], lw[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-            hw[e] = split2(fmaxf(v[2 * e], 0.f) * sy, fmaxf(v[2 * e + 1], 0.f) * sy, lw[e]);
-        uint8_t* dst = Yc + (size_t)u * BLK + q * 128 + rr * 16;
-        *reinterpret_cast<uint4*>(dst) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-        *reinterpret_cast<uint4*>(dst + 512) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        ypart[blockIdx.x] = t;
+        if (c) atomicAdd(nclamp, c);
     }
 }
 
@@ -199,22 +195,17 @@ bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p) {
 cudaError_t nmf_mma_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
                             unsigned* status, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    cudaError_t e = nmf_tc_stats(g, p, w, Y, ld_y, status, s);
-    if (e != cudaSuccess) return e;
-    k_mma_convert<<<g.num_sms * 16, 256, 0, s>>>(Y, ld_y, Np, g.Nk, p.mma_NB, p.mma_Npad / MR, w.ymax,
-                                                  static_cast<uint8_t*>(w.Yc));
+    k_mma_prep<YSrc><<<p.nby, 256, 0, s>>>(YSrc{Y, ld_y}, Np, g.Nk, p.mma_NB, p.mma_Npad / MR,
+                                          static_cast<uint8_t*>(w.Yc), w.texp, w.ypart, status, w.nclamp);
     return cudaGetLastError();
 }
 
 cudaError_t nmf_mma_prepare_counts(const Geometry& g, const NmfPlan& p, const NmfWs& w, const DeviceTables& t,
                                    const CountsIn& cin, unsigned* status, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    const CountsSrc C{cin.y, cin.y0, cin.b, t.logtab, (int64_t)g.Nr * g.Nc, g.Nk};
-    cudaError_t e = cudaMemsetAsync(w.ymax, 0, 2 * sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
-    k_mma_counts_stats<<<p.nby, 256, 0, s>>>(C, Np, w.ymax, w.ypart, status, w.nclamp);
-    k_mma_counts_convert<<<g.num_sms * 16, 256, 0, s>>>(C, Np, p.mma_NB, p.mma_Npad / MR, w.ymax,
-                                                         static_cast<uint8_t*>(w.Yc));
+    CSrc src{cin.y, cin.y0, cin.b, t.logtab, (int64_t)g.Nr * g.Nc, nullptr, 0, 0};
+    k_mma_prep<CSrc><<<p.nby, 256, 0, s>>>(src, Np, g.Nk, p.mma_NB, p.mma_Npad / MR, static_cast<uint8_t*>(w.Yc),
+                                          w.texp, w.ypart, status, w.nclamp);
     return cudaGetLastError();
 }
 

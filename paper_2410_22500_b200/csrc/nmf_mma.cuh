@@ -27,8 +27,8 @@
 //
 // Precision (R20): the same fp16 hi/lo split as the tcgen05 pass: x = (hi + lo)/s,
 // |error| <= 2^-22 |x| in the normal range, power-of-two scales s with s max < 2^14 -- one per
-// call for Y+, one per component and warp (bin range) for D, one per component and tile for
-// V.  Three MMAs per block (hi.hi + hi.lo + lo.hi; lo.lo is below 2^-22).  Phase-1
+// 16-row tile for Y+ (k_mma_prep), one per component and warp (bin range) for D, one per
+// component and tile for V.  Three MMAs per block (hi.hi + hi.lo + lo.hi; lo.lo is below 2^-22).  Phase-1
 // accumulators run over one warp's 13 blocks; phase-2 accumulators cover one block of one tile
 // and are added to the fp32 register sums with their scale (FFMA), so no tensor-core sum is
 // longer than 39 MMAs.  Cross-warp and cross-CTA sums are fp32 / fp64 in a fixed order:
@@ -62,7 +62,7 @@ struct MmaArgs {
     float* Bpart;         // [nCTA][K][Nkp]
     double* Hpart;        // [nCTA][K*K]
     double* vpart;        // [nCTA][2]
-    const unsigned* ymax; // bits of max Y+ (k_tc_stats)
+    const int* texp;      // [ntiles] exponent of each tile's Y+ scale sigma_Y = 2^texp (k_mma_prep)
     unsigned* status;
     int it;               // iteration index (one pass per launch)
     // persistent launch: all n_iter iterations with the D update between passes
@@ -192,8 +192,6 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             mbar_arrive_cta(&vfull[s]);
         }
     };
-    const int ey = mexp(__uint_as_float(*A.ymax));
-    const float isy = pow2(-ey);
     // phase-2 ldmatrix.trans: lanes 8i..8i+7 address core matrix (0, 2, 1, 3)[i]
     const unsigned toff = (unsigned)((((lane >> 3) == 1) ? 2 : ((lane >> 3) == 2) ? 1 : (lane >> 3)) * 128 +
                                      (lane & 7) * 16);
@@ -236,7 +234,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             __syncthreads();
         }
         uint32_t dh[NBW][NC][2], dl[NBW][NC][2];
-        float invA[NC][2];  // 1 / (sigma_Y sigma_D[k]) for this lane's output columns k = 2t, 2t + 1 (+ 8 nc)
+        float invA[NC][2];  // 1 / sigma_D[k] for this lane's output columns k = 2t, 2t + 1 (+ 8 nc)
 #pragma unroll
         for (int nc = 0; nc < NC; ++nc) {
             const int kd = g + 8 * nc;
@@ -259,8 +257,8 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                 dh[j][nc][0] = split2(dv[j][0] * sd, dv[j][1] * sd, dl[j][nc][0]);
                 dh[j][nc][1] = split2(dv[j][2] * sd, dv[j][3] * sd, dl[j][nc][1]);
             }
-            invA[nc][0] = isy * pow2(-__shfl_sync(0xffffffffu, ed, 8 * t));
-            invA[nc][1] = isy * pow2(-__shfl_sync(0xffffffffu, ed, 8 * t + 4));
+            invA[nc][0] = pow2(-__shfl_sync(0xffffffffu, ed, 8 * t));  // (x 1 / sigma_Y of the tile)
+            invA[nc][1] = pow2(-__shfl_sync(0xffffffffu, ed, 8 * t + 4));
         }
 
         float bacc[NBW][NC][4];
@@ -272,14 +270,18 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                 for (int e = 0; e < 4; ++e) bacc[j][nc][e] = 0.f;
         double vdotA = 0.0;
         unsigned bad = 0;
+        int ety = nmine > 0 ? __ldg(A.texp + tile_of(0, fwd)) : 0;  // tile scale exponent (k_mma_prep)
 
         for (int64_t m = 0; m < nmine; ++m) {
             const int64_t n = n0 + m;
             const int s = (int)(n % MNS);
             const unsigned par = (unsigned)((n / MNS) & 1);
             const int sv4 = (int)(n % MNV);
-            const int64_t r0 = tile_of(m, fwd) * MR;
+            const int64_t tile = tile_of(m, fwd), r0 = tile * MR;
             const int nv = (int)min((int64_t)MR, A.Np - r0);
+            const float isy = pow2(-ety);  // 1 / sigma_Y of the tile
+            // the next tile's exponent, one tile ahead (an L2 load's latency exceeds phase 1)
+            ety = m + 1 < nmine ? __ldg(A.texp + tile_of(m + 1, fwd)) : 0;
             mbar_wait(&full[warp][s], par);
             const unsigned sb = ringw + (unsigned)(s * slotb);
             // ---- phase 1: this warp's partial A = Y+_R D^T over its blocks.  Straight-line code
@@ -309,10 +311,11 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
                 float* rb = red + (size_t)(((n & 1) * MW + warp) * NC + nc) * 128;
-                rb[wo0] = (a0[nc][0] + (a1[nc][0] + a2[nc][0])) * invA[nc][0];
-                rb[wo1] = (a0[nc][1] + (a1[nc][1] + a2[nc][1])) * invA[nc][1];
-                rb[wo0 + 2] = (a0[nc][2] + (a1[nc][2] + a2[nc][2])) * invA[nc][0];
-                rb[wo1 + 2] = (a0[nc][3] + (a1[nc][3] + a2[nc][3])) * invA[nc][1];
+                const float i0 = invA[nc][0] * isy, i1 = invA[nc][1] * isy;
+                rb[wo0] = (a0[nc][0] + (a1[nc][0] + a2[nc][0])) * i0;
+                rb[wo1] = (a0[nc][1] + (a1[nc][1] + a2[nc][1])) * i1;
+                rb[wo0 + 2] = (a0[nc][2] + (a1[nc][2] + a2[nc][2])) * i0;
+                rb[wo1 + 2] = (a0[nc][3] + (a1[nc][3] + a2[nc][3])) * i1;
             }
             // V G and the old V of this lane's (row, component) pairs -- before the barrier, so no
             // warp can still be reading old V rows of a ragged tile (global memory) once the
@@ -657,7 +660,7 @@ cudaError_t mma_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* 
     A.Bpart = w.Bpart;
     A.Hpart = w.Hpart;
     A.vpart = w.vpart;
-    A.ymax = w.ymax;
+    A.texp = w.texp;
     A.status = status;
     A.it = it;
     A.n_iter = n_iter;

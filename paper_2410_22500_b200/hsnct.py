@@ -116,6 +116,10 @@ def lib():
             L.hsnct_debug_fbp_timing.restype = i32
             L.hsnct_debug_fbp_times.argtypes = [vp, vp]
             L.hsnct_debug_fbp_times.restype = i32
+            L.hsnct_debug_nmf_timing.argtypes = [vp, ctypes.c_int]
+            L.hsnct_debug_nmf_timing.restype = i32
+            L.hsnct_debug_nmf_times.argtypes = [vp, vp]
+            L.hsnct_debug_nmf_times.restype = i32
             L.hsnct_abi_version.argtypes = []
             L.hsnct_abi_version.restype = i32
             _lib = L
@@ -480,6 +484,16 @@ class Hsnct:
         """(ramp filter ms, backprojection ms) of the last timed fbp call (waits for it)."""
         ms = (ctypes.c_float * 2)()
         _check(lib().hsnct_debug_fbp_times(self._h, ctypes.cast(ms, ctypes.c_void_p)))
+        return float(ms[0]), float(ms[1])
+
+    def debug_nmf_timing(self, on: bool):
+        """Record CUDA events around the input preparation and the iterations of later decompose calls."""
+        _check(lib().hsnct_debug_nmf_timing(self._h, 1 if on else 0))
+
+    def debug_nmf_times(self):
+        """(input preparation ms, iterations ms) of the last timed decompose call (waits for it)."""
+        ms = (ctypes.c_float * 2)()
+        _check(lib().hsnct_debug_nmf_times(self._h, ctypes.cast(ms, ctypes.c_void_p)))
         return float(ms[0]), float(ms[1])
 
     def debug_trace(self):

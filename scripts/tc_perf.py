@@ -49,8 +49,10 @@ def main():
             h.sync()
             return e0.elapsed_time(e1), V, D
         ms1, _, _ = timed(1)
+        nh = max(1, n_iter // 2)
+        msh, _, _ = timed(nh)
         ms, V, D = timed(n_iter)
-        it_ms = (ms - ms1) / max(1, n_iter - 1)  # marginal cost of one iteration (no input prep)
+        it_ms = (ms - msh) / max(1, n_iter - nh)  # marginal cost of one iteration (no input prep)
         by = n_iter * (4.0 * cfg.Np * cfg.Nk + 8.0 * cfg.Np * cfg.K)
         gbs = by / (ms * 1e-3) / 1e9
         gbi = (4.0 * cfg.Np * cfg.Nk + 8.0 * cfg.Np * cfg.K) / (it_ms * 1e-3) / 1e9

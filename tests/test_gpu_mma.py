@@ -156,3 +156,29 @@ def test_mma_scale_invariance(mm):
         res.append((V.cpu() / np.sqrt(s), D.cpu() / np.sqrt(s)))
     for V, D in res[1:]:
         assert rel(V, res[0][0].numpy()) <= 1e-5 and rel(D, res[0][1].numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("plan", ["mma", "ffma"])
+def test_nmf_stage_timing(monkeypatch, plan):
+    """hsnct_debug_nmf_timing/_times: events around the input preparation and the iterations
+    (the persistent launch), same result as an untimed call."""
+    monkeypatch.setenv("HSNCT_NMF", plan)
+    from paper_2410_22500_b200 import Hsnct, HsnctError
+    cfg = sd.custom(idx=79, Nc=32, Nv=16, Nr=2, Nk=400, K=5, M=4)
+    pr = sd.make_problem(cfg)
+    h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
+    Y = pr["Y"].to(DEV)
+    out = []
+    for timed in (False, True):
+        V, D = pr["V0"].to(DEV).clone(), pr["D0"].to(DEV).clone()
+        h.debug_nmf_timing(timed)
+        h.subspace_decompose(Y, V, D, 6)
+        if timed:
+            prep_ms, it_ms = h.debug_nmf_times()
+            assert prep_ms > 0 and it_ms > 0
+        h.sync()
+        out.append((V.cpu(), D.cpu()))
+    h.debug_nmf_timing(False)
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    with pytest.raises(HsnctError):
+        h.debug_nmf_times()
