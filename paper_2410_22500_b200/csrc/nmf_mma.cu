@@ -40,6 +40,7 @@ struct CSrc {
     const float* b;      // [Nv][Nk] or null
     const double* Lg;    // [256] (device table)
     int64_t NrNc;
+    int vec;             // N_k % 8 == 0 and y, y0 8-byte, b 16-byte aligned
     const double* L;     // the table in shared memory (stage)
     int64_t v0, rc0;     // view and (r, c) index of the current tile's first row
     __device__ void stage(double* Ls) {
@@ -61,6 +62,25 @@ struct CSrc {
         const uint8_t* yr = y + r * Nk;
         const uint8_t* y0r = y0 + rc * Nk;
         const float* br = b ? b + vv * Nk : nullptr;
+        if (vec && r < Np && l + 8 <= Nk) {  // 8-byte count loads, 16-byte offset loads
+            const uint2 a = LAST ? __ldcs(reinterpret_cast<const uint2*>(yr + l)) : __ldg(reinterpret_cast<const uint2*>(yr + l));
+            const uint2 o = __ldg(reinterpret_cast<const uint2*>(y0r + l));
+            float bb[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (br) {
+                const float4 b0 = __ldg(reinterpret_cast<const float4*>(br + l)), b1 = __ldg(reinterpret_cast<const float4*>(br + l) + 1);
+                bb[0] = b0.x; bb[1] = b0.y; bb[2] = b0.z; bb[3] = b0.w;
+                bb[4] = b1.x; bb[5] = b1.y; bb[6] = b1.z; bb[7] = b1.w;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const unsigned ye = ((e < 4 ? a.x : a.y) >> (8 * (e & 3))) & 0xffu;
+                const unsigned oe = ((e < 4 ? o.x : o.y) >> (8 * (e & 3))) & 0xffu;
+                double d = L[oe] - L[ye];
+                if (br) d -= (double)bb[e];
+                v[e] = (float)d;
+            }
+            return;
+        }
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             float f = 0.f;
@@ -203,7 +223,10 @@ cudaError_t nmf_mma_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w,
 cudaError_t nmf_mma_prepare_counts(const Geometry& g, const NmfPlan& p, const NmfWs& w, const DeviceTables& t,
                                    const CountsIn& cin, unsigned* status, cudaStream_t s) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    CSrc src{cin.y, cin.y0, cin.b, t.logtab, (int64_t)g.Nr * g.Nc, nullptr, 0, 0};
+    const bool vec = g.Nk % 8 == 0 && (reinterpret_cast<uintptr_t>(cin.y) & 7) == 0 &&
+                     (reinterpret_cast<uintptr_t>(cin.y0) & 7) == 0 &&
+                     (cin.b == nullptr || (reinterpret_cast<uintptr_t>(cin.b) & 15) == 0);
+    CSrc src{cin.y, cin.y0, cin.b, t.logtab, (int64_t)g.Nr * g.Nc, vec ? 1 : 0, nullptr, 0, 0};
     k_mma_prep<CSrc><<<p.nby, 256, 0, s>>>(src, Np, g.Nk, p.mma_NB, p.mma_Npad / MR, static_cast<uint8_t*>(w.Yc),
                                           w.texp, w.ypart, status, w.nclamp);
     return cudaGetLastError();

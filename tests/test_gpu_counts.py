@@ -63,6 +63,7 @@ def test_generator_counts_decode_bitwise():
     ("twopass", sd.custom(idx=55, Nc=20, Nv=13, Nk=203, K=5, M=4, counts=30.0)),
     ("tc", sd.CONFIGS[1]),
     ("mma", sd.custom(idx=56, Nc=20, Nv=13, Nk=203, K=5, M=4, counts=30.0)),
+    ("mma", sd.custom(idx=57, Nc=24, Nv=10, Nr=3, Nk=400, K=6, M=4, counts=20.0)),  # vector decode (N_k % 8 == 0)
 ])
 def test_decompose_counts_bitwise(monkeypatch, plan, cfg):
     if plan == "nopersist":
