@@ -182,3 +182,30 @@ def test_nmf_stage_timing(monkeypatch, plan):
     assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
     with pytest.raises(HsnctError):
         h.debug_nmf_times()
+
+
+def test_mma_per_iteration_launches_match_persistent(monkeypatch):
+    """HSNCT_NO_PERSIST=1: the same pass as one launch per iteration + k_dred (the path taken
+    when the cooperative launch is refused, by the sharded row pass, and for K*K + K*SL > 256);
+    against the oracle and against the persistent launch (same row-pass arithmetic, different
+    reduction order in the D update)."""
+    cfg = sd.custom(idx=80, Nc=32, Nv=16, Nr=2, Nk=800, K=6, M=5)
+    pr = sd.make_problem(cfg)
+    monkeypatch.setenv("HSNCT_NMF", "mma")
+    from paper_2410_22500_b200 import Hsnct
+    res = []
+    for nop in ("0", "1"):
+        monkeypatch.setenv("HSNCT_NO_PERSIST", nop)
+        h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
+        assert ("PERSIST=1" in h.debug_plan()) == (nop == "0"), h.debug_plan()
+        V, D = pr["V0"].to(DEV).clone(), pr["D0"].to(DEV).clone()
+        obj = torch.zeros(40, dtype=torch.float64, device=DEV)
+        h.subspace_decompose(pr["Y"].to(DEV), V, D, 20, obj_trace=obj)
+        h.sync()
+        res.append((V, D, obj))
+        h.close()
+    Vo, Do, objo = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), 20, objective=True)
+    for V, D, obj in res:
+        assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3
+        np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
+    assert rel(res[0][0], res[1][0].cpu().double().numpy()) <= 1e-5
