@@ -143,6 +143,15 @@ template <int K, int NBW, bool PERSIST>
 __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
     static_assert(K >= 1 && K <= 16, "two n8 column blocks at most");
     constexpr int NC = mma_nc(K);
+    // DISTV: the V update computed once per tile (warp w: components w and w + 8, lane: row
+    // lane % 16) and shared through shared memory with a second barrier, instead of redundantly in
+    // every warp (C5: 2.7% per iteration in steady state, fewer instructions under the power cap).
+    // HSNCT_MMA_NODISTV builds the redundant version (A/B).
+#ifdef HSNCT_MMA_NODISTV
+    constexpr bool DISTV = false;
+#else
+    constexpr bool DISTV = true;
+#endif
     constexpr int KK = K * K;
     constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [2 NC values][NC column blocks][32 lanes]
     extern __shared__ __align__(128) uint8_t smem[];
@@ -152,7 +161,8 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
     __shared__ double vsh[MW];
     __shared__ double Hs[KK], Gold[KK], Gnew[KK];
     __shared__ double red8[MW];
-    __shared__ float Gf[NC == 1 ? 1 : 16 * K];  // NC = 2: G as float [j][16] (the V update's V G)
+    __shared__ float Gf[(NC == 1 && !DISTV) ? 1 : 16 * K];  // G as float [j][16] (the V update's V G)
+    __shared__ float vnew_s[DISTV ? 8 * NC * MR : 1];        // DISTV: the tile's new V [k][row]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int c = blockIdx.x, nC = gridDim.x;
     const size_t slotb = (size_t)NBW * BLK;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
         // between the passes of a persistent launch: L2 loads (__ldcg), G from shared memory.
         // (NC = 2: from a float copy in shared memory, to save the registers)
         float gcol[NC == 1 ? K : 1];
-        if constexpr (NC == 1) {
+        if constexpr (NC == 1 && !DISTV) {
 #pragma unroll
             for (int j = 0; j < K; ++j) gcol[j] = g < K ? (float)Gold[j * K + g] : 0.f;
         } else {
@@ -320,9 +330,15 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             // V G and the old V of this lane's (row, component) pairs -- before the barrier, so no
             // warp can still be reading old V rows of a ragged tile (global memory) once the
             // tile's owner warp stores the new ones
-            mbar_wait(&vfull[sv4], (unsigned)((n / MNV) & 1));
             float vg[NC][4], vo[NC][4];
-            {
+            if constexpr (DISTV) {
+                // old V rows of a ragged tile into its (unused) V slot, read after the barrier
+                if (nv < MR && warp == 0) {
+                    float* vs = vrows + (size_t)sv4 * MR * K;
+                    for (int i = lane; i < nv * K; i += 32) vs[i] = A.V[r0 * K + i];
+                }
+            } else {
+                mbar_wait(&vfull[sv4], (unsigned)((n / MNV) & 1));
                 const float* vr = nv == MR ? vrows + (size_t)sv4 * MR * K : A.V + r0 * K;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -355,8 +371,48 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             uint32_t vh0[NC], vh1[NC], vl0[NC], vl1[NC];
             int evs[NC];
             float invB[NC][2], ivB[NC][2];
+            if constexpr (DISTV) {
+                mbar_wait(&vfull[sv4], (unsigned)((n / MNV) & 1));
+                const int k = warp + 8 * (lane >> 4), r = lane & 15;  // component, tile row
+                if (k < K) {
+                    const int kk = k & 7, u = (r & 7) >> 1, e = (r & 1) + 2 * (r >> 3);
+                    const float* rd = red + (size_t)((n & 1) * MW * NC + (k >> 3)) * 128 + ((4 * kk + u) ^ (kk >> 1)) * 4 + e;
+                    float a = rd[0];
+#pragma unroll
+                    for (int w = 1; w < MW; ++w) a += rd[w * NC * 128];
+                    const float* vr = vrows + (size_t)sv4 * MR * K + r * K;
+                    float x = 0.f, v0 = 0.f;
+                    if (r < nv) {
+#pragma unroll
+                        for (int j = 0; j < K; ++j) {
+                            const float vj = vr[j];
+                            x = fmaf(vj, Gf[j * 16 + k], x);
+                            if (j == k) v0 = vj;
+                        }
+                    }
+                    const float vnk = a * (v0 * rcp_approx(fmaxf(x, 1e-30f)));
+                    vnew_s[k * MR + r] = vnk;
+                    if (r < nv) {
+                        if (first && !(isfinite(v0) && v0 >= 0.f)) bad |= ST_INIT_BAD;
+                        if (!isfinite(vnk)) bad |= ST_NUMERIC;
+                        A.V[(r0 + r) * K + k] = vnk;
+                        vdotA += (double)(vnk * a);
+                    }
+                }
+                named_bar(2, MTH);
+            }
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
+              if constexpr (DISTV) {
+                const int kd = g + 8 * nc;
+                const float2 p0 = kd < K ? *reinterpret_cast<const float2*>(&vnew_s[kd * MR + 2 * t]) : make_float2(0.f, 0.f);
+                const float2 p1 = kd < K ? *reinterpret_cast<const float2*>(&vnew_s[kd * MR + 2 * t + 8]) : make_float2(0.f, 0.f);
+                vn[nc][0] = p0.x;
+                vn[nc][1] = p0.y;
+                vn[nc][2] = p1.x;
+                vn[nc][3] = p1.y;
+                av[nc][0] = av[nc][1] = av[nc][2] = av[nc][3] = 0.f;
+              } else {
                 const float4* rd =
                     reinterpret_cast<const float4*>(red + (size_t)(((n & 1) * MW) * NC + nc) * 128) + rsl;
                 float4 s4 = rd[0];
@@ -372,14 +428,16 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                 av[nc][1] = s4.y;
                 av[nc][2] = s4.z;
                 av[nc][3] = s4.w;
-                float vmax = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     // V / max(VG, 1e-30) by the approximate reciprocal (the divisor is a normal
                     // number; 1 ulp); rows and components outside the tile have vo = 0
                     vn[nc][e] = av[nc][e] * (vo[nc][e] * rcp_approx(fmaxf(vg[nc][e], 1e-30f)));
-                    vmax = fmaxf(vmax, fabsf(vn[nc][e]));
                 }
+              }
+                float vmax = 0.f;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) vmax = fmaxf(vmax, fabsf(vn[nc][e]));
                 vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 1));
                 vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, 2));
                 const int ev = mexp(vmax);
@@ -394,6 +452,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             }
             if (warp == (int)(m % MW)) {  // this tile's V store, <V_new, A>, H += V_new^T V_new
                 float va = 0.f;
+                if constexpr (!DISTV)
 #pragma unroll
                 for (int nc = 0; nc < NC; ++nc)
 #pragma unroll
@@ -406,7 +465,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                             va = fmaf(vn[nc][e], av[nc][e], va);
                         }
                     }
-                vdotA += (double)va;
+                if constexpr (!DISTV) vdotA += (double)va;
                 // H on the tensor core: A operand V^T (rows g, g + 8: this lane's B-operand
                 // fragments of column blocks 0 and 1), B operand V (column block nb2):
                 // C[g (+8)][2t + i + 8 nb2] = sum_r V[r][.] V[r][.], scaled by sigma_V sigma_V
