@@ -555,9 +555,13 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                   "input_bytes_fp32": 4 * cfg.Np * cfg.Nk, "input_bytes_counts": cfg.Np * cfg.Nk + cfg.Nr * cfg.Nc * cfg.Nk,
                   "note": "hsnct_subspace_decompose_counts: Eq. 2 decoded inside the Y+ preparation; the "
                           "iterations read the fp32 Y+ as before (bit-identical V, D)"}
+        counts["note"] = ("hsnct_subspace_decompose_counts: Eq. 2 decoded inside the input preparation; the "
+                          "iterations read the prepared operand as before (bit-identical V, D)")
         del yc, y0c
-        pr.pop("y", None)
-        pr.pop("y0", None)
+    # host copies of the counts for the counts-domain end-to-end line (NEXT-1 e2e)
+    ych = (pr["y"].cpu(), pr["y0"].cpu()) if (not args.no_e2e and "y" in pr) else None
+    pr.pop("y", None)
+    pr.pop("y0", None)
 
     # end to end through the public API on page-locked HOST buffers (hsnct_fhr_stream): the
     # timed region holds, every step, the H2D copy of Y, V0, D0, the three stages, and the D2H
@@ -601,7 +605,33 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
                "steps": n_e2e, "window_slices": wsl,
                "path": "hsnct_fhr_stream (H2D, decompose, fbp, windowed synthesis + D2H into a pinned ring)",
                "timer": "host wall clock around the blocking call (max over ranks)"}
-        del ws_e, ring, Yh
+        del ws_e, Yh
+        # the same end to end from the detector counts (hsnct_fhr_stream_counts): H2D of uint8 y, y0
+        # (1 + 1/N_v bytes per element) instead of fp32 Y; Eq. 2 decoded on the device
+        if ych is not None:
+            yh, y0h = ych[0].pin_memory(), ych[1].pin_memory()
+            ych = None
+            ws_c = torch.empty(hm2.lib().hsnct_fhr_stream_counts_bytes(h._h, wsl), dtype=torch.uint8, device=dev)
+            h.fhr_stream_counts(yh, y0h, V0h, D0h, n_iter, window_slices=wsl, ring=ring, on_window=on_window,
+                                V=Vh, D=Dh, ws=ws_c)  # warm-up
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            got[0] = 0
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                h.fhr_stream_counts(yh, y0h, V0h, D0h, n_iter, window_slices=wsl, ring=ring, on_window=on_window,
+                                    V=Vh, D=Dh, ws=ws_c)
+            t_c = max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
+            assert got[0] == n_e2e * cfg.Nr
+            e2e["counts_input"] = {
+                "value": cfg.Nx * cfg.Nk * world / t_c, "unit": UNIT, "ms_per_step": t_c * 1e3,
+                "h2d_bytes_per_step": Np * Nk + cfg.Nr * cfg.Nc * Nk + 4 * (Np * K + K * Nk),
+                "d2h_bytes_per_step": 4 * (Nx * Nk + Np * K + K * Nk), "steps": n_e2e,
+                "path": "hsnct_fhr_stream_counts (H2D of uint8 y, y0, Eq. 2 in the decomposition's input "
+                        "preparation, then as hsnct_fhr_stream)"}
+            del ws_c, yh, y0h
+        del ring
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:  # the CPU baseline: rank 0 at N = 1 only

@@ -255,6 +255,18 @@ hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, cons
                               hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
                               void* ws, size_t ws_bytes, void* stream);
 
+/* hsnct_fhr_stream from the detector counts (NEXT-1 end to end; Eq. 2, with the
+ * Appendix-A offset): the HOST arrays y_host uint8 [N_p][N_k], y0_host uint8
+ * [N_r N_c][N_k] and b_host fp32 [N_v][N_k] (nullable: b = 0) go to the device (1 + 1/N_v bytes
+ * per element instead of 4) and the decomposition decodes Y = fp32((L[y0] - L[y]) - b) as
+ * hsnct_subspace_decompose_counts does -- the results equal hsnct_fhr_stream's on the decoded Y
+ * bit for bit.  Everything else as hsnct_fhr_stream; workspace hsnct_fhr_stream_counts_bytes. */
+size_t hsnct_fhr_stream_counts_bytes(hsnct_t h, int window_slices);
+hsnct_status hsnct_fhr_stream_counts(hsnct_t h, const uint8_t* y_host, const uint8_t* y0_host, const float* b_host,
+                                     const float* V0_host, const float* D0_host, int n_iter, int window_slices,
+                                     float* ring_host, hsnct_window_fn on_window, void* user, float* V_host,
+                                     float* D_host, void* ws, size_t ws_bytes, void* stream);
+
 /* ---- Fast material decomposition, semi-supervised back half (NEXT-2):
  * Algorithm 2 after the subspace reconstruction, on X
  * [K][N_x] (hsnct_fbp's output).  1 <= n_mat <= min(K, 8).  Workspace:

@@ -166,6 +166,14 @@ FhrHostLayout stream_layout(const Geometry& g, const NmfPlan& p, int window_slic
     return L;
 }
 
+// hsnct_fhr_stream_counts: stream_layout; the counts y, y0, b live in the Y region when the plan
+// decodes them in its input preparation (fused, mma), else behind it
+size_t stream_counts_bytes(const Geometry& g, const NmfPlan& p, int window_slices) {
+    const FhrHostLayout L = stream_layout(g, p, window_slices);
+    const size_t cb = a256((size_t)Np_of(g) * g.Nk) + a256((size_t)g.Nr * g.Nc * g.Nk) + a256((size_t)g.Nv * g.Nk * 4);
+    return (p.fused || p.mma) ? L.total + (cb > L.y ? cb - L.y : 0) : L.total + cb;
+}
+
 hsnct_status check_ws(void* ws, size_t have, size_t need, const char* op) {
     if (need == 0) return HSNCT_OK;
     if (!ws) return fail(HSNCT_E_ARG, "%s: workspace is NULL (need %zu bytes)", op, need);
@@ -762,22 +770,29 @@ size_t hsnct_fhr_stream_bytes(hsnct_t h, int window_slices) {
     return stream_layout(h->g, h->nmf, std::min(window_slices, h->g.Nr)).total;
 }
 
-hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
-                              const float* D0_host, int n_iter, int window_slices, float* ring_host,
-                              hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
-                              void* ws, size_t ws_bytes, void* stream) {
-    Nvtx nvtx_("hsnct_fhr_stream");
+}  // extern "C"
+
+// hsnct_fhr_stream (Y_host, ld_y) and hsnct_fhr_stream_counts (ch: host counts, Eq. 2 on the device)
+static hsnct_status fhr_stream_impl(hsnct_t h, const float* Y_host, int64_t ld_y, const CountsIn* ch,
+                                    const float* V0_host, const float* D0_host, int n_iter, int window_slices,
+                                    float* ring_host, hsnct_window_fn on_window, void* user, float* V_host,
+                                    float* D_host, void* ws, size_t ws_bytes, void* stream) {
     g_last_error.clear();
     if (!h) return fail(HSNCT_E_ARG, "fhr_stream: handle is NULL");
     const Geometry& g = h->g;
-    if (!Y_host || !V0_host || !D0_host || !ring_host)
-        return fail(HSNCT_E_ARG, "fhr_stream: Y, V0, D0 and the ring are required");
-    if (ld_y < g.Nk) return fail(HSNCT_E_ARG, "fhr_stream: ld_y=%lld < N_k=%d", (long long)ld_y, g.Nk);
+    if ((!Y_host && !ch) || !V0_host || !D0_host || !ring_host)
+        return fail(HSNCT_E_ARG, "fhr_stream: Y (or y, y0), V0, D0 and the ring are required");
+    if (ch) {
+        hsnct_status sc = check_counts(g, ch->y, ch->y0, ch->b, "fhr_stream_counts");
+        if (sc) return sc;
+    } else if (ld_y < g.Nk) {
+        return fail(HSNCT_E_ARG, "fhr_stream: ld_y=%lld < N_k=%d", (long long)ld_y, g.Nk);
+    }
     if (n_iter < 0) return fail(HSNCT_E_ARG, "fhr_stream: n_iter=%d < 0", n_iter);
     if (window_slices < 1) return fail(HSNCT_E_ARG, "fhr_stream: window_slices=%d < 1", window_slices);
     const int wsl = std::min(window_slices, g.Nr);
     const FhrHostLayout L = stream_layout(g, h->nmf, wsl);
-    hsnct_status st = check_ws(ws, ws_bytes, L.total, "fhr_stream");
+    hsnct_status st = check_ws(ws, ws_bytes, ch ? stream_counts_bytes(g, h->nmf, wsl) : L.total, "fhr_stream");
     if (st) return st;
     DeviceGuard guard(h->device);
     cudaStream_t s = (cudaStream_t)stream;
@@ -803,12 +818,40 @@ hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, cons
     c += L.nmf;
     void* wf = c;
     const int64_t Np = Np_of(g);
-    CK(cudaMemcpy2DAsync(Yd, (size_t)L.Nkp * sizeof(float), Y_host, (size_t)ld_y * sizeof(float),
-                         (size_t)g.Nk * sizeof(float), (size_t)Np, cudaMemcpyHostToDevice, s),
-       "fhr_stream H2D Y");
+    if (!ch) {
+        CK(cudaMemcpy2DAsync(Yd, (size_t)L.Nkp * sizeof(float), Y_host, (size_t)ld_y * sizeof(float),
+                             (size_t)g.Nk * sizeof(float), (size_t)Np, cudaMemcpyHostToDevice, s),
+           "fhr_stream H2D Y");
+    }
     CK(cudaMemcpyAsync(Vd, V0_host, (size_t)Np * g.K * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_stream H2D V0");
     CK(cudaMemcpyAsync(Dd, D0_host, (size_t)g.K * g.Nk * sizeof(float), cudaMemcpyHostToDevice, s), "fhr_stream H2D D0");
-    if ((st = run_decompose(h, Yd, L.Nkp, Vd, Dd, n_iter, nullptr, wn, s))) return st;
+    if (ch) {
+        // the counts (1 + 1/N_v bytes per element) in the Y region when the plan decodes them in its
+        // input preparation, else behind the workspace (and decoded into the Y region first)
+        const bool inprep = h->nmf.fused || h->nmf.mma;
+        const size_t ny = (size_t)Np * g.Nk, ny0 = (size_t)g.Nr * g.Nc * g.Nk;
+        char* cb = inprep ? reinterpret_cast<char*>(Yd) : static_cast<char*>(ws) + L.total;
+        uint8_t* yd = reinterpret_cast<uint8_t*>(cb);
+        uint8_t* y0d = yd + a256(ny);
+        float* bd = ch->b ? reinterpret_cast<float*>(y0d + a256(ny0)) : nullptr;
+        CK(cudaMemcpyAsync(yd, ch->y, ny, cudaMemcpyHostToDevice, s), "fhr_stream_counts H2D y");
+        CK(cudaMemcpyAsync(y0d, ch->y0, ny0, cudaMemcpyHostToDevice, s), "fhr_stream_counts H2D y0");
+        if (bd)
+            CK(cudaMemcpyAsync(bd, ch->b, (size_t)g.Nv * g.Nk * sizeof(float), cudaMemcpyHostToDevice, s),
+               "fhr_stream_counts H2D b");
+        const CountsIn cin{yd, y0d, bd};
+        if (inprep) {
+            if ((st = run_decompose(h, nullptr, 0, Vd, Dd, n_iter, nullptr, wn, s, &cin))) return st;
+        } else {
+            CK(counts_decode(g, h->t, cin, Yd, L.Nkp, 0, h->nmf.nby > 0 ? h->nmf.nby : g.num_sms * 8, nullptr,
+                             nullptr, s),
+               "fhr_stream_counts decode");
+            h->launches += 1;
+            if ((st = run_decompose(h, Yd, L.Nkp, Vd, Dd, n_iter, nullptr, wn, s))) return st;
+        }
+    } else if ((st = run_decompose(h, Yd, L.Nkp, Vd, Dd, n_iter, nullptr, wn, s))) {
+        return st;
+    }
     if ((st = run_fbp(h, Vd, Xd, wf, s))) return st;
     if (V_host)
         CK(cudaMemcpyAsync(V_host, Vd, (size_t)Np * g.K * sizeof(float), cudaMemcpyDeviceToHost, s), "fhr_stream D2H V");
@@ -844,6 +887,32 @@ hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, cons
     CK(cudaStreamWaitEvent(s, h->ev_cpy[(nwin - 1) & 1], 0), "fhr_stream order");
     if (nwin >= 2) CK(cudaStreamWaitEvent(s, h->ev_cpy[(nwin - 2) & 1], 0), "fhr_stream order");
     return read_status(h, s);
+}
+
+extern "C" {
+
+hsnct_status hsnct_fhr_stream(hsnct_t h, const float* Y_host, int64_t ld_y, const float* V0_host,
+                              const float* D0_host, int n_iter, int window_slices, float* ring_host,
+                              hsnct_window_fn on_window, void* user, float* V_host, float* D_host,
+                              void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fhr_stream");
+    return fhr_stream_impl(h, Y_host, ld_y, nullptr, V0_host, D0_host, n_iter, window_slices, ring_host, on_window,
+                           user, V_host, D_host, ws, ws_bytes, stream);
+}
+
+size_t hsnct_fhr_stream_counts_bytes(hsnct_t h, int window_slices) {
+    if (!h || window_slices < 1) return 0;
+    return stream_counts_bytes(h->g, h->nmf, std::min(window_slices, h->g.Nr));
+}
+
+hsnct_status hsnct_fhr_stream_counts(hsnct_t h, const uint8_t* y_host, const uint8_t* y0_host, const float* b_host,
+                                     const float* V0_host, const float* D0_host, int n_iter, int window_slices,
+                                     float* ring_host, hsnct_window_fn on_window, void* user, float* V_host,
+                                     float* D_host, void* ws, size_t ws_bytes, void* stream) {
+    Nvtx nvtx_("hsnct_fhr_stream_counts");
+    const CountsIn ch{y_host, y0_host, b_host};
+    return fhr_stream_impl(h, nullptr, 0, &ch, V0_host, D0_host, n_iter, window_slices, ring_host, on_window, user,
+                           V_host, D_host, ws, ws_bytes, stream);
 }
 
 static hsnct_status check_nmat(const Geometry& g, int n_mat, const char* op) {

@@ -84,6 +84,11 @@ def lib():
             L.hsnct_fhr_stream_bytes.restype = sz
             L.hsnct_fhr_stream.argtypes = [vp, vp, i64, vp, vp, i32, i32, vp, WINDOW_FN, vp, vp, vp, vp, sz, vp]
             L.hsnct_fhr_stream.restype = i32
+            L.hsnct_fhr_stream_counts_bytes.argtypes = [vp, i32]
+            L.hsnct_fhr_stream_counts_bytes.restype = sz
+            L.hsnct_fhr_stream_counts.argtypes = [vp, vp, vp, vp, vp, vp, i32, i32, vp, WINDOW_FN, vp, vp, vp, vp,
+                                                  sz, vp]
+            L.hsnct_fhr_stream_counts.restype = i32
             L.hsnct_sync.argtypes = [vp, vp]
             L.hsnct_sync.restype = i32
             L.hsnct_kernel_launches.argtypes = [vp]
@@ -389,11 +394,30 @@ class Hsnct:
         (hsnct_fhr_stream).  on_window(slice0, n_slices, xh) is called on this thread for every
         window as soon as it is on the host; xh is a [n_slices*N_c*N_c, N_k] view into the ring,
         valid only during the call.  Blocks until the last window has been delivered."""
-        for t, name in ((Y, "Y"), (V0, "V0"), (D0, "D0")):
-            if t.device.type != "cpu" or t.dtype != torch.float32:
-                raise HsnctError(E_ARG, f"{name} must be a float32 host tensor")
+        if Y.device.type != "cpu" or Y.dtype != torch.float32:
+            raise HsnctError(E_ARG, "Y must be a float32 host tensor")
         if Y.dim() != 2 or Y.shape != (self.Np, self.Nk) or Y.stride(1) != 1:
             raise HsnctError(E_ARG, "Y must be [N_p, N_k] with unit column stride")
+        return self._fhr_stream(("Y", Y), V0, D0, n_iter, window_slices, ring, on_window, V, D, ws, stream)
+
+    def fhr_stream_counts(self, y, y0, V0, D0, n_iter, b=None, window_slices=None, ring=None, on_window=None,
+                          V=None, D=None, ws=None, stream=None):
+        """fhr_stream from the detector counts (hsnct_fhr_stream_counts, NEXT-1 end to end): HOST
+        uint8 y [N_p, N_k] and y0 [N_r*N_c, N_k], optional fp32 offset b [N_v, N_k]; Eq. 2 is
+        decoded on the device.  Results equal fhr_stream on the decoded Y."""
+        for t, name, shape in ((y, "y", (self.Np, self.Nk)), (y0, "y0", (self.Nr * self.Nc, self.Nk))):
+            if t.device.type != "cpu" or t.dtype != torch.uint8 or tuple(t.shape) != shape or not t.is_contiguous():
+                raise HsnctError(E_ARG, f"{name} must be a contiguous uint8 host tensor {shape}")
+        if b is not None and (b.device.type != "cpu" or b.dtype != torch.float32 or
+                              tuple(b.shape) != (self.Nv, self.Nk) or not b.is_contiguous()):
+            raise HsnctError(E_ARG, "b must be a contiguous float32 host tensor [N_v, N_k]")
+        return self._fhr_stream(("counts", (y, y0, b)), V0, D0, n_iter, window_slices, ring, on_window, V, D, ws,
+                                stream)
+
+    def _fhr_stream(self, src, V0, D0, n_iter, window_slices, ring, on_window, V, D, ws, stream):
+        for t, name in ((V0, "V0"), (D0, "D0")):
+            if t.device.type != "cpu" or t.dtype != torch.float32:
+                raise HsnctError(E_ARG, f"{name} must be a float32 host tensor")
         V0 = V0.contiguous()
         D0 = D0.contiguous()
         wsl = self.fhr_stream_window_slices() if window_slices is None else int(window_slices)
@@ -402,8 +426,11 @@ class Hsnct:
             ring = self.fhr_stream_ring(wsl)
         if not ring.is_contiguous() or ring.numel() < 2 * wsl * self.Nc * self.Nc * self.Nk or ring.device.type != "cpu":
             raise HsnctError(E_ARG, "ring must be a contiguous host tensor of two windows")
+        L = lib()
+        counts = src[0] == "counts"
         if ws is None:
-            ws = torch.empty(lib().hsnct_fhr_stream_bytes(self._h, wsl), dtype=torch.uint8, device=self.device)
+            nb = (L.hsnct_fhr_stream_counts_bytes if counts else L.hsnct_fhr_stream_bytes)(self._h, wsl)
+            ws = torch.empty(nb, dtype=torch.uint8, device=self.device)
         per = self.Nc * self.Nc * self.Nk
         base = ring.data_ptr()
         flat = ring.reshape(-1)
@@ -418,9 +445,17 @@ class Hsnct:
                 err.append(e)
 
         fn = WINDOW_FN(cb)
-        _check(lib().hsnct_fhr_stream(self._h, _ptr(Y), Y.stride(0), _ptr(V0), _ptr(D0), int(n_iter), wsl,
-                                      _ptr(ring), fn, None, _ptr(V), _ptr(D), _ptr(ws),
-                                      ws.numel() * ws.element_size(), _stream(stream, self.device)))
+        nbytes = ws.numel() * ws.element_size()
+        if counts:
+            y, y0, b = src[1]
+            _check(L.hsnct_fhr_stream_counts(self._h, _ptr(y), _ptr(y0), _ptr(b), _ptr(V0), _ptr(D0), int(n_iter),
+                                             wsl, _ptr(ring), fn, None, _ptr(V), _ptr(D), _ptr(ws), nbytes,
+                                             _stream(stream, self.device)))
+        else:
+            Y = src[1]
+            _check(L.hsnct_fhr_stream(self._h, _ptr(Y), Y.stride(0), _ptr(V0), _ptr(D0), int(n_iter), wsl,
+                                      _ptr(ring), fn, None, _ptr(V), _ptr(D), _ptr(ws), nbytes,
+                                      _stream(stream, self.device)))
         if err:
             raise err[0]
         return ring

@@ -30,7 +30,7 @@ def test_header_declares_the_boundary():
               "hsnct_fbp", "hsnct_synthesize", "hsnct_dhr", "hsnct_fhr_host", "hsnct_sync",
               "hsnct_status_string", "hsnct_last_error", "hsnct_kernel_launches", "hsnct_abi_version",
               "hsnct_fmd_transform", "hsnct_fmd_materials", "hsnct_fmd_spectra", "hsnct_debug_trace",
-              "hsnct_debug_fbp_timing", "hsnct_debug_fbp_times", "hsnct_debug_nmf_timing",
+              "hsnct_debug_fbp_timing", "hsnct_debug_fbp_times", "hsnct_debug_nmf_timing", "hsnct_fhr_stream_counts",
               "hsnct_debug_nmf_times"):
         assert s in syms
 

@@ -115,3 +115,39 @@ def test_counts_errors():
     with pytest.raises(HsnctError):
         h.counts_to_projections(y.to(DEV), y0.to(DEV)[:-1])
     h.close()
+
+
+@pytest.mark.parametrize("plan", [None, "mma", "twopass"])
+def test_fhr_stream_counts_equals_fhr_stream(monkeypatch, plan):
+    """hsnct_fhr_stream_counts (NEXT-1 end to end): host uint8 counts and the offset b in, Eq. 2
+    on the device; every x^h window and V, D equal hsnct_fhr_stream on the decoded Y bit for bit
+    (plans that decode in their preparation, and the two-pass plan that decodes into a Y buffer)."""
+    if plan is not None:
+        monkeypatch.setenv("HSNCT_NMF", plan)
+    from paper_2410_22500_b200 import Hsnct
+    cfg = sd.custom(idx=58, Nc=24, Nv=10, Nr=3, Nk=96, K=4, M=3, counts=20.0)
+    pr = sd.make_problem(cfg, return_counts=True)
+    h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
+    b = (0.05 * torch.randn((cfg.Nv, cfg.Nk), generator=torch.Generator().manual_seed(4))).float()
+    Ybuf = torch.empty((cfg.Np, (cfg.Nk + 3) // 4 * 4), dtype=torch.float32, device=DEV)
+    Y = h.counts_to_projections(pr["y"].to(DEV), pr["y0"].to(DEV), b.to(DEV), Y=Ybuf[:, :cfg.Nk]).cpu()
+    out = {}
+    for mode in ("Y", "counts"):
+        wins = []
+        Vh, Dh = torch.empty_like(pr["V0"]), torch.empty_like(pr["D0"])
+
+        def on_window(s0, ns, xh):
+            wins.append((s0, ns, xh.clone()))
+        if mode == "Y":
+            h.fhr_stream(Y.pin_memory(), pr["V0"], pr["D0"], 12, window_slices=2, on_window=on_window, V=Vh, D=Dh)
+        else:
+            h.fhr_stream_counts(pr["y"].pin_memory(), pr["y0"].pin_memory(), pr["V0"], pr["D0"], 12, b=b.pin_memory(),
+                                window_slices=2, on_window=on_window, V=Vh, D=Dh)
+        out[mode] = (wins, Vh, Dh)
+    (w1, V1, D1), (w2, V2, D2) = out["Y"], out["counts"]
+    print(h.debug_plan())
+    assert torch.equal(V1, V2) and torch.equal(D1, D2)
+    assert [(s, n) for s, n, _ in w1] == [(s, n) for s, n, _ in w2] == [(0, 2), (2, 1)]
+    for (_, _, x1), (_, _, x2) in zip(w1, w2):
+        assert torch.equal(x1, x2)
+    h.close()
