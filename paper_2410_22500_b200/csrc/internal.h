@@ -174,10 +174,6 @@ cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
                            unsigned* status, cudaStream_t s);
 cudaError_t nmf_tc_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                           unsigned* status, cudaStream_t s);
-// max(Y+), max row norm, ||Y+||^2 partials, non-finite check, clamped count (k_tc_stats; tc and
-// mma paths)
-cudaError_t nmf_tc_stats(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
-                         unsigned* status, cudaStream_t s);
 // mma.sync path: plan (mma_* fields, nblk_f, nby), input preparation, one row pass
 bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p);
 cudaError_t nmf_mma_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,

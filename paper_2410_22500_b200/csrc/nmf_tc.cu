@@ -841,15 +841,6 @@ cudaError_t nmf_tc_prepare(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
     return cudaGetLastError();
 }
 
-cudaError_t nmf_tc_stats(const Geometry& g, const NmfPlan& p, const NmfWs& w, const float* Y, int64_t ld_y,
-                         unsigned* status, cudaStream_t s) {
-    const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
-    cudaError_t e = cudaMemsetAsync(w.ymax, 0, 2 * sizeof(unsigned), s);
-    if (e != cudaSuccess) return e;
-    k_tc_stats<<<p.nby, 256, 0, s>>>(Y, ld_y, Np, g.Nk, w.ymax, w.ymax + 1, w.ypart, status, w.nclamp);
-    return cudaGetLastError();
-}
-
 cudaError_t nmf_tc_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                           unsigned* status, cudaStream_t s) {
     switch (g.K) {

@@ -209,3 +209,18 @@ def test_mma_per_iteration_launches_match_persistent(monkeypatch):
         assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3
         np.testing.assert_allclose(obj.cpu().numpy(), objo, rtol=1e-3)
     assert rel(res[0][0], res[1][0].cpu().double().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("Nc,Nv,Nr,Nk,K", [(3, 2, 1, 5, 2), (4, 3, 1, 17, 1), (5, 3, 1, 33, 9)])
+def test_mma_degenerate_shapes(mm, Nc, Nv, Nr, Nk, K):
+    """Fewer rows than one 16-row tile (one ragged tile, one CTA), N_k below one 16-bin block per
+    warp, K = 1 and two column blocks with a single extra component."""
+    cfg = sd.custom(idx=90 + Nc, Nc=Nc, Nv=Nv, Nr=Nr, Nk=Nk, K=K, M=min(K, 2))
+    pr = sd.make_problem(cfg)
+    h = mm(cfg)
+    V = pr["V0"].to(DEV).clone()
+    D = pr["D0"].to(DEV).clone()
+    h.subspace_decompose(padded(pr["Y"], (Nk + 3) // 4 * 4), V, D, 8)
+    h.sync()
+    Vo, Do = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), 8)
+    assert rel(V, Vo) <= 1e-4 and rel(D, Do) <= 1e-4, (rel(V, Vo), rel(D, Do))
