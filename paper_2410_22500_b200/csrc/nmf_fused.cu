@@ -57,6 +57,8 @@ bool nmf_fused_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const int64_t ntiles = (Np + RG - 1) / RG;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));
+    const char* nbk = getenv("HSNCT_NBLK");  // A/B: fewer persistent CTAs (grid barrier / partial count)
+    if (nbk && atoi(nbk) > 0) p->nblk_f = std::min(p->nblk_f, atoi(nbk));
     p->PB = p->nblk_f;
     // the persistent kernel's D update gives every CTA a lambda slice of SL = ceil(Nk / nCTA)
     // bins: dnew holds 64 per component, the fp64 B slice SCR/2 values, and threads

@@ -77,12 +77,29 @@ def test_create_rejects_bad_geometry(L):
     from paper_2410_22500_b200.hsnct import _Geom
     h = ctypes.c_void_p()
     bad = [(1, 1, 16, 8, 2), (8, 0, 16, 8, 2), (8, 1, 1, 8, 2), (8, 1, 2048, 8, 2), (8, 1, 16, 0, 1),
-           (8, 1, 16, 8, 0), (8, 1, 16, 8, 17), (8, 1, 16, 4, 5), (8, 1, 16, 8000, 16)]
+           (8, 1, 16, 8, 0), (8, 1, 16, 8, 17), (8, 1, 16, 4, 5), (8, 1, 16, 8000, 16),
+           (8, 1, 1025, 8, 2), (8, 1, 16, 3201, 16)]  # just past the N_c and K*N_kp limits
     for nv, nr, nc, nk, k in bad:
         g = _Geom(nv, nr, nc, nk, k, None)
         assert L.hsnct_create(ctypes.byref(g), 0, ctypes.byref(h)) == 1, (nv, nr, nc, nk, k)
         assert h.value is None
     assert L.hsnct_create(None, 0, ctypes.byref(h)) == 1
+
+
+def test_create_accepts_the_limits(L):
+    """N_c = 1024 and K * round_up(N_k, 4) = 51200 pass the argument checks (include/hsnct.h);
+    without a GPU the call then fails on the device query (HSNCT_E_CUDA), not HSNCT_E_ARG."""
+    import torch
+    from paper_2410_22500_b200.hsnct import _Geom
+    for nv, nr, nc, nk, k in [(8, 1, 1024, 8, 2), (8, 1, 16, 3200, 16), (2, 1, 2, 1, 1)]:
+        h = ctypes.c_void_p()
+        g = _Geom(nv, nr, nc, nk, k, None)
+        rc = L.hsnct_create(ctypes.byref(g), 0, ctypes.byref(h))
+        if torch.cuda.is_available():
+            assert rc == 0, (nv, nr, nc, nk, k, L.hsnct_last_error())
+            L.hsnct_destroy(h)
+        else:
+            assert rc == 4, (nv, nr, nc, nk, k, rc, L.hsnct_last_error())
 
 
 def test_create_without_gpu_reports_cuda(L):
