@@ -27,12 +27,21 @@ def handle(cfg):
     return Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
 
 
+def padded(Y):
+    """Y on the device in rows of ld = round_up(N_k, 4) floats (the boundary's ld rule), the
+    padding NaN-poisoned (must be ignored)."""
+    Np, Nk = Y.shape
+    buf = torch.full((Np, (Nk + 3) // 4 * 4), float("nan"), dtype=torch.float32, device=DEV)
+    buf[:, :Nk] = Y.to(DEV)
+    return buf[:, :Nk]
+
+
 def pipeline(cfg, n_iter):
     pr = sd.make_problem(cfg)
     h = handle(cfg)
     V = pr["V0"].to(DEV).clone()
     D = pr["D0"].to(DEV).clone()
-    h.subspace_decompose(pr["Y"].to(DEV), V, D, n_iter)
+    h.subspace_decompose(padded(pr["Y"]), V, D, n_iter)
     X = h.fbp(V)
     Xh = h.synthesize(X, D)
     h.sync()
