@@ -18,7 +18,7 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhsnct.so")
 BUILD = os.path.join(HERE, "build")
 
-SOURCES = (["api.cpp", "nmf.cu", "nmf_fused.cu", "nmf_tc.cu", "nmf_mma.cu", "nmf_mma_lo.cu", "nmf_mma_hi.cu", "fbp.cu", "synth.cu", "fmd.cu", "mbir.cu", "counts.cu"]
+SOURCES = (["api.cpp", "nmf.cu", "nmf_fused.cu", "nmf_tc.cu", "nmf_mma.cu", "nmf_mma_lo.cu", "nmf_mma_hi.cu", "nmf_mma_hi16.cu", "fbp.cu", "synth.cu", "fmd.cu", "mbir.cu", "counts.cu"]
            + [f"nmf_fused_k{k}.cu" for k in range(1, 17)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

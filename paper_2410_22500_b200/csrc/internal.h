@@ -106,7 +106,8 @@ struct NmfPlan {
     // mma.sync row pass (nmf_mma.cu), K <= 8: one launch per iteration + k_dred
     bool mma;
     int mma_NB;      // 16-bin blocks per row = ceil(Nk / 16)
-    int mma_NBW;     // blocks per warp (template instance >= ceil(NB / 8))
+    int mma_NBW;     // blocks per warp (template instance >= ceil(NB / mma_MW))
+    int mma_MW;      // warps per CTA: 8, or 16 (K = 9..16 with HSNCT_MMA_MW=16)
     int64_t mma_Npad;// Np rounded up to the 16-row tile
     // two-pass fallback (nmf.cu)
     int nblk_v, nchunk, bthreads, nlam_blk;

@@ -878,8 +878,9 @@ std::string nmf_plan_desc(const Geometry& g, const NmfPlan& p) {
                  TC_CLUSTER, TC_CLUSTER * p.tc_ncl, p.tc_R, p.tc_R2, p.tc_rg.W, p.tc_rg.L[TC_CLUSTER - 1],
                  p.tc_rg.L[0]);
     else if (p.mma)
-        snprintf(b, sizeof b, "mma k_nmf_mma<K=%d,NBW=%d,PERSIST=%d> grid=%d 16-row tiles, %d blocks/row%s", g.K,
-                 p.mma_NBW, p.persist ? 1 : 0, p.nblk_f, p.mma_NB, p.persist ? "" : " +k_dred");
+        snprintf(b, sizeof b, "mma k_nmf_mma<K=%d,NBW=%d,PERSIST=%d%s> grid=%d 16-row tiles, %d blocks/row%s", g.K,
+                 p.mma_NBW, p.persist ? 1 : 0, p.mma_MW == 16 ? ",MW=16" : "", p.nblk_f, p.mma_NB,
+                 p.persist ? "" : " +k_dred");
     else if (p.persist)
         snprintf(b, sizeof b, "persist k_nmf_persist<K=%d,LP=%d,NBG=%d,NGRP=%d> grid=%d", g.K, p.LP, p.nbuf,
                  p.ngrp, p.nblk_f);

@@ -173,10 +173,16 @@ __global__ void __launch_bounds__(256) k_mma_prep(Src src, int64_t Np, int Nk, i
     }
 }
 
-// blocks per warp instantiated: the smallest of these >= ceil(NB / 8)
+// blocks per warp instantiated: the smallest of these >= ceil(NB / warps)
 constexpr int NBW_SET[] = {2, 4, 6, 8, 10, 13};
-int nbw_of(int NB) {
-    const int need = (NB + MW - 1) / MW;
+constexpr int NBW_SET16[] = {1, 2, 3, 4, 5};
+int nbw_of(int NB, int mw) {
+    const int need = (NB + mw - 1) / mw;
+    if (mw == MW16) {
+        for (int v : NBW_SET16)
+            if (v >= need) return v;
+        return 0;
+    }
     for (int v : NBW_SET)
         if (v >= need) return v;
     return 0;
@@ -187,13 +193,24 @@ int nbw_of(int NB) {
 bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     if (g.K > 16) return false;
     const int NB = (g.Nk + 15) / 16;
-    const int nbw = nbw_of(NB);
+    // K = 9..16 (two column blocks): 8 warps with <= 10 blocks each (255 registers); HSNCT_MMA_MW=16
+    // selects the 16-warp form (<= 5 blocks per warp, 128 registers, four warps per scheduler),
+    // measured slower at C6 (12.1 vs 10.4 ms per iteration: the per-warp, per-tile work -- partial-A
+    // exchange, operand loads, barriers -- is paid 16 times; profiles/r02/session4/ab_split.txt)
+    int mw = MW;
+    if (g.K > 8) {
+        const char* e = getenv("HSNCT_MMA_MW");
+        if (e && atoi(e) == 16) mw = MW16;
+    }
+    const int nbw = nbw_of(NB, mw);
     if (!nbw) return false;
     if (g.K > 8 && nbw > 10) return false;  // two column blocks: registers for <= 10 blocks per warp
-    const size_t smem = mma_smem_bytes(nbw, g.K);
-    // static part: mbarriers, the per-warp H accumulators [8 NC]^2, H / G_old / G_new, sums
+    const size_t smem = mma_smem_bytes(nbw, g.K, mw);
+    // static part: mbarriers, the H accumulators of 8 warps [8 NC]^2, H / G_old / G_new, G as
+    // float, the tile's new V, sums
     const size_t nc = (size_t)mma_nc(g.K), KK = (size_t)g.K * g.K;
-    const size_t stat = 8 * (MW * MNS + MNV) + 8 * MW * 64 * nc * nc + 8 * MW * 2 + 24 * KK + 256;
+    const size_t stat = 8 * ((size_t)mw * MNS + MNV) + 8 * 8 * 64 * nc * nc + 8 * (size_t)mw * 2 + 24 * KK +
+                        4 * 16 * (size_t)g.K + 4 * 8 * nc * MR + 256;
     if (smem + stat + 1024 > (size_t)232448) return false;  // 227 KB per block (1 KB reserved)
     const int64_t Np = (int64_t)g.Nv * g.Nr * g.Nc;
     const int64_t ntiles = (Np + MR - 1) / MR;
@@ -202,10 +219,11 @@ bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     {
         const int nC = (int)std::max<int64_t>(1, std::min<int64_t>((Np + MR - 1) / MR, (int64_t)num_sms));
         const int SL = (g.Nk + nC - 1) / nC;
-        p->persist_fits = SL <= 64 && g.K * SL <= 256 && g.K * g.K + g.K * SL <= MTH;
+        p->persist_fits = SL <= 64 && g.K * SL <= 256 && g.K * g.K + g.K * SL <= mw * 32;
     }
     p->mma_NB = NB;
     p->mma_NBW = nbw;
+    p->mma_MW = mw;
     p->mma_Npad = ntiles * MR;
     p->nblk_f = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));
     p->nby = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 8, (Np + 7) / 8));
@@ -234,24 +252,42 @@ cudaError_t nmf_mma_prepare_counts(const Geometry& g, const NmfPlan& p, const Nm
 
 cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, const float* D, int it,
                            unsigned* status, cudaStream_t s) {
-    switch (g.K) {
 #define M(KV) \
     case KV: return mma_launch_k<KV, false>(g, p, w, V, const_cast<float*>(D), it, 1, nullptr, nullptr, status, s);
+#define M16(KV) \
+    case KV: return mma_launch_k16<KV, false>(g, p, w, V, const_cast<float*>(D), it, 1, nullptr, nullptr, status, s);
+    if (p.mma_MW == MW16) {
+        switch (g.K) {
+            HSNCT_MMA_KHI(M16)
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    switch (g.K) {
         HSNCT_MMA_K(M)
-#undef M
         default: return cudaErrorInvalidValue;
     }
+#undef M16
+#undef M
 }
 
 cudaError_t nmf_mma_persist_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D,
                                    int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
-    switch (g.K) {
 #define M(KV) \
     case KV: return mma_launch_k<KV, true>(g, p, w, V, D, 0, n_iter, obj, bar, status, s);
+#define M16(KV) \
+    case KV: return mma_launch_k16<KV, true>(g, p, w, V, D, 0, n_iter, obj, bar, status, s);
+    if (p.mma_MW == MW16) {
+        switch (g.K) {
+            HSNCT_MMA_KHI(M16)
+            default: return cudaErrorInvalidValue;
+        }
+    }
+    switch (g.K) {
         HSNCT_MMA_K(M)
-#undef M
         default: return cudaErrorInvalidValue;
     }
+#undef M16
+#undef M
 }
 
 }  // namespace hsnct

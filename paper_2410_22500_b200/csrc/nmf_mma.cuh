@@ -120,14 +120,20 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 
 // Column blocks of 8 components: NC = 1 (K <= 8) or 2 (K = 9..16)
 __host__ __device__ constexpr int mma_nc(int K) { return (K + 7) / 8; }
-// Dynamic shared memory: ring [MW][MNS][NBW*BLK] | old V rows [MNV][MR*K] | partial A
-// [2][MW][NC][32 reader lanes][4]
-__host__ __device__ constexpr size_t mma_vrows_off(int NBW) { return (size_t)MW * MNS * NBW * BLK; }
-__host__ __device__ constexpr size_t mma_red_off(int NBW, int K) {
-    return mma_vrows_off(NBW) + (((size_t)MNV * MR * K * 4 + 15) & ~(size_t)15);
+// Warps per CTA (= bin ranges of a tile): 8, or 16 (MW16: two column blocks with half the blocks
+// per warp, so that the per-warp state fits 128 registers and four warps share a scheduler)
+constexpr int MW16 = 16;
+// Partial-A buffers: two (a warp may write tile m + 1's partials while others still read tile
+// m's), one with 16 warps (the V update's second barrier already orders them; shared memory)
+__host__ __device__ constexpr int mma_nrb(int mw) { return mw == MW16 ? 1 : 2; }
+// Dynamic shared memory: ring [mw][MNS][NBW*BLK] | old V rows [MNV][MR*K] | partial A
+// [nrb][mw][NC][32 reader lanes][4]
+__host__ __device__ constexpr size_t mma_vrows_off(int NBW, int mw = MW) { return (size_t)mw * MNS * NBW * BLK; }
+__host__ __device__ constexpr size_t mma_red_off(int NBW, int K, int mw = MW) {
+    return mma_vrows_off(NBW, mw) + (((size_t)MNV * MR * K * 4 + 15) & ~(size_t)15);
 }
-__host__ __device__ constexpr size_t mma_smem_bytes(int NBW, int K) {
-    return mma_red_off(NBW, K) + (size_t)2 * MW * mma_nc(K) * 128 * 4;
+__host__ __device__ constexpr size_t mma_smem_bytes(int NBW, int K, int mw = MW) {
+    return mma_red_off(NBW, K, mw) + (size_t)mma_nrb(mw) * mw * mma_nc(K) * 128 * 4;
 }
 
 // The row pass (one iteration's V half-step and the B, H, <V_new, A> partials of each CTA) and,
@@ -139,9 +145,13 @@ __host__ __device__ constexpr size_t mma_smem_bytes(int NBW, int K) {
 // <V_new, A> terms are taken by warp m % 8 (every warp holds the whole new V of the tile).
 // Components: NC column blocks of 8 (K = 9..16: every MMA of the pass and every per-lane
 // V-update value twice, once per block).
-template <int K, int NBW, bool PERSIST>
-__global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
+template <int K, int NBW, bool PERSIST, int MWT = 8>
+__global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
     static_assert(K >= 1 && K <= 16, "two n8 column blocks at most");
+    static_assert(MWT == 8 || (MWT == MW16 && mma_nc(K) == 2), "8 warps, or 16 with two column blocks");
+    constexpr int MW = MWT, MTH = MWT * 32;  // (shadow the 8-warp constants)
+    constexpr int MHW = 8;                   // warps that own tiles' H / <V, A> terms (m % 8)
+    constexpr int NRB = mma_nrb(MWT);
     constexpr int NC = mma_nc(K);
     // DISTV: the V update computed once per tile (warp w: components w and w + 8, lane: row
     // lane % 16) and shared through shared memory with a second barrier, instead of redundantly in
@@ -152,23 +162,28 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
 #else
     constexpr bool DISTV = true;
 #endif
+    static_assert(DISTV || MWT == 8, "16 warps: the per-tile V update only");
     constexpr int KK = K * K;
     constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [2 NC values][NC column blocks][32 lanes]
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t full[MW][MNS];
     __shared__ uint64_t vfull[MNV];
-    __shared__ double hsh[MW][HW];
+    __shared__ double hsh[MHW][HW];
     __shared__ double vsh[MW];
     __shared__ double Hs[KK], Gold[KK], Gnew[KK];
     __shared__ double red8[MW];
     __shared__ float Gf[(NC == 1 && !DISTV) ? 1 : 16 * K];  // G as float [j][16] (the V update's V G)
-    __shared__ float vnew_s[DISTV ? 8 * NC * MR : 1];        // DISTV: the tile's new V [k][row]
+    // DISTV: the tile's new V as the phase-2 B operand, split once by the V update's threads:
+    // [component][t][vh0, vh1, vl0, vl1] (one 16-byte load per lane and column block), and the
+    // exponents of the per-component scales sigma_V (zero for components >= K)
+    __shared__ __align__(16) uint32_t vfrag_s[DISTV ? 8 * NC * 16 : 4];
+    __shared__ __align__(8) int ev_s[DISTV ? 8 * NC : 2];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int c = blockIdx.x, nC = gridDim.x;
     const size_t slotb = (size_t)NBW * BLK;
     uint8_t* ring = smem;
-    float* vrows = reinterpret_cast<float*>(smem + mma_vrows_off(NBW));
-    float* red = reinterpret_cast<float*>(smem + mma_red_off(NBW, K));
+    float* vrows = reinterpret_cast<float*>(smem + mma_vrows_off(NBW, MW));
+    float* red = reinterpret_cast<float*>(smem + mma_red_off(NBW, K, MW));
     const int jb = warp * A.NB / MW, nb = (warp + 1) * A.NB / MW - jb;
     const int64_t ntiles = (A.Np + MR - 1) / MR;
     const int64_t nmine = ntiles > c ? (ntiles - 1 - c) / nC + 1 : 0;
@@ -212,7 +227,12 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
     const int wsl0 = 8 * t + ((g >> 1) ^ t), wsl1 = 8 * t + 4 + ((g >> 1) ^ t);
     const int wo0 = 4 * wsl0 + (g & 1), wo1 = 4 * wsl1 + (g & 1);
     const int rsl = lane ^ (g >> 1);  // this lane's read slot (k = g, u = t)
-    for (int i = lane; i < HW; i += 32) hsh[warp][i] = 0.0;
+    if (warp < MHW)
+        for (int i = lane; i < HW; i += 32) hsh[warp][i] = 0.0;
+    if constexpr (DISTV) {
+        for (int i = tid; i < 8 * NC * 16; i += MTH) vfrag_s[i] = 0u;
+        for (int i = tid; i < 8 * NC; i += MTH) ev_s[i] = 0;
+    }
 
     // D update slice of this CTA (PERSIST)
     const int SL = (A.Nk + nC - 1) / nC;
@@ -320,7 +340,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             }
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
-                float* rb = red + (size_t)(((n & 1) * MW + warp) * NC + nc) * 128;
+                float* rb = red + (size_t)(((n & (NRB - 1)) * MW + warp) * NC + nc) * 128;
                 const float i0 = invA[nc][0] * isy, i1 = invA[nc][1] * isy;
                 rb[wo0] = (a0[nc][0] + (a1[nc][0] + a2[nc][0])) * i0;
                 rb[wo1] = (a0[nc][1] + (a1[nc][1] + a2[nc][1])) * i1;
@@ -373,13 +393,16 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             float invB[NC][2], ivB[NC][2];
             if constexpr (DISTV) {
                 mbar_wait(&vfull[sv4], (unsigned)((n / MNV) & 1));
-                const int k = warp + 8 * (lane >> 4), r = lane & 15;  // component, tile row
+                // component, tile row (16 warps: the half-warps sum warps 0-7 and 8-15's partials)
+                const int k = MW == MW16 ? warp : warp + 8 * (lane >> 4), r = lane & 15;
                 if (k < K) {
                     const int kk = k & 7, u = (r & 7) >> 1, e = (r & 1) + 2 * (r >> 3);
-                    const float* rd = red + (size_t)((n & 1) * MW * NC + (k >> 3)) * 128 + ((4 * kk + u) ^ (kk >> 1)) * 4 + e;
+                    const float* rd = red + (size_t)((n & (NRB - 1)) * MW * NC + (k >> 3)) * 128 + ((4 * kk + u) ^ (kk >> 1)) * 4 + e;
+                    if constexpr (MW == MW16) rd += (lane >> 4) * 8 * NC * 128;
                     float a = rd[0];
 #pragma unroll
-                    for (int w = 1; w < MW; ++w) a += rd[w * NC * 128];
+                    for (int w = 1; w < 8; ++w) a += rd[w * NC * 128];
+                    if constexpr (MW == MW16) a += __shfl_xor_sync(0xffffffffu, a, 16);
                     const float* vr = vrows + (size_t)sv4 * MR * K + r * K;
                     float x = 0.f, v0 = 0.f;
                     if (r < nv) {
@@ -391,8 +414,22 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                         }
                     }
                     const float vnk = a * (v0 * rcp_approx(fmaxf(x, 1e-30f)));
-                    vnew_s[k * MR + r] = vnk;
-                    if (r < nv) {
+                    {   // sigma_V of the component over the tile's 16 rows (this half-warp), hi/lo split
+                        const unsigned hm = (lane & 16) ? 0xffff0000u : 0x0000ffffu;
+                        float vmax = fabsf(vnk);
+#pragma unroll
+                        for (int o = 1; o < 16; o <<= 1) vmax = fmaxf(vmax, __shfl_xor_sync(hm, vmax, o));
+                        const int ev = mexp(vmax);
+                        const float xs = vnk * pow2(ev);
+                        const __half hh = __float2half_rn(xs);
+                        const __half hl = __float2half_rn(xs - __half2float(hh));
+                        // row r = 2 t + i (+ 8): half i of word (r >> 3) (hi) / 2 + (r >> 3) (lo)
+                        __half* fr = reinterpret_cast<__half*>(vfrag_s) + ((k * 4 + u) * 4 + (r >> 3)) * 2 + (r & 1);
+                        fr[0] = hh;
+                        fr[4] = hl;
+                        if (r == 0) ev_s[k] = ev;
+                    }
+                    if (r < nv && (MW == 8 || lane < 16)) {
                         if (first && !(isfinite(v0) && v0 >= 0.f)) bad |= ST_INIT_BAD;
                         if (!isfinite(vnk)) bad |= ST_NUMERIC;
                         A.V[(r0 + r) * K + k] = vnk;
@@ -404,14 +441,17 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
               if constexpr (DISTV) {
-                const int kd = g + 8 * nc;
-                const float2 p0 = kd < K ? *reinterpret_cast<const float2*>(&vnew_s[kd * MR + 2 * t]) : make_float2(0.f, 0.f);
-                const float2 p1 = kd < K ? *reinterpret_cast<const float2*>(&vnew_s[kd * MR + 2 * t + 8]) : make_float2(0.f, 0.f);
-                vn[nc][0] = p0.x;
-                vn[nc][1] = p0.y;
-                vn[nc][2] = p1.x;
-                vn[nc][3] = p1.y;
-                av[nc][0] = av[nc][1] = av[nc][2] = av[nc][3] = 0.f;
+                const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(8 * nc * 4 + lane) * 4]);
+                vh0[nc] = f.x;
+                vh1[nc] = f.y;
+                vl0[nc] = f.z;
+                vl1[nc] = f.w;
+                evs[nc] = ev_s[g + 8 * nc];
+                const int2 e2 = *reinterpret_cast<const int2*>(&ev_s[2 * t + 8 * nc]);
+                ivB[nc][0] = pow2(-e2.x);  // 1 / sigma_V[k], k = 2t (+ 8 nc)
+                ivB[nc][1] = pow2(-e2.y);
+                invB[nc][0] = isy * ivB[nc][0];
+                invB[nc][1] = isy * ivB[nc][1];
               } else {
                 const float4* rd =
                     reinterpret_cast<const float4*>(red + (size_t)(((n & 1) * MW) * NC + nc) * 128) + rsl;
@@ -434,7 +474,6 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                     // number; 1 ulp); rows and components outside the tile have vo = 0
                     vn[nc][e] = av[nc][e] * (vo[nc][e] * rcp_approx(fmaxf(vg[nc][e], 1e-30f)));
                 }
-              }
                 float vmax = 0.f;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) vmax = fmaxf(vmax, fabsf(vn[nc][e]));
@@ -449,8 +488,9 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
                 ivB[nc][1] = pow2(-__shfl_sync(0xffffffffu, ev, 8 * t + 4));
                 invB[nc][0] = isy * ivB[nc][0];
                 invB[nc][1] = isy * ivB[nc][1];
+              }
             }
-            if (warp == (int)(m % MW)) {  // this tile's V store, <V_new, A>, H += V_new^T V_new
+            if (warp == (int)(m % MHW)) {  // this tile's V store, <V_new, A>, H += V_new^T V_new
                 float va = 0.f;
                 if constexpr (!DISTV)
 #pragma unroll
@@ -557,7 +597,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             // H[ka][kb] is the sum of lane 4 (ka % 8) + (kb % 8) / 2's value q = 2 (ka / 8) + kb % 2,
             // column block kb / 8
             const int hi = ((2 * (ka >> 3) + (kb & 1)) * NC + (kb >> 3)) * 32 + 4 * (ka & 7) + ((kb & 7) >> 1);
-            for (int w = 0; w < MW; ++w) h += hsh[w][hi];
+            for (int w = 0; w < MHW; ++w) h += hsh[w][hi];
             A.Hpart[(int64_t)c * KK + tid] = h;
         }
         if (tid == 0) {
@@ -567,7 +607,8 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             A.vpart[2 * (int64_t)c + 1] = 0.0;
         }
         __syncthreads();  // hsh read before it is cleared for the next pass
-        for (int i = lane; i < HW; i += 32) hsh[warp][i] = 0.0;
+        if (warp < MHW)
+            for (int i = lane; i < HW; i += 32) hsh[warp][i] = 0.0;
         if constexpr (PERSIST) {
             // the next pass's old-V head rows (written by this pass: generic stores, fenced above)
             if (it + 1 < it_end && tid == 0) {
@@ -579,7 +620,7 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
             //      and D_new D_new^T slice partials -> grid barrier -> G_new, objective
             double* gacc = reinterpret_cast<double*>(red);  // the partial-A buffers are idle here
             double* Bsl = gacc + MTH;                        // [K * nsl]  (<= 256)
-            double* dnew = Bsl + 256;                        // [K][64] (the buffers hold 2048 NC doubles)
+            double* dnew = Bsl + 256;                        // [K][64] (the buffers hold >= 1024 NC doubles)
             grid_sync(A.bar, epoch);
             const bool objcta = c == nC - 1 && (A.obj || it == 0);
             double va = 0.0;
@@ -700,12 +741,13 @@ __global__ void __launch_bounds__(MTH, 1) k_nmf_mma(MmaArgs A) {
         for (int o = tid; o < KK; o += MTH) A.Gd[o] = Gold[o];
 }
 
-template <int K, int NBW, bool PERSIST>
+template <int K, int NBW, bool PERSIST, int MWT = 8>
 cudaError_t mma_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int it, int n_iter,
                     double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
     static SmemAttr attr;
-    const size_t smem = mma_smem_bytes(NBW, K);
-    cudaError_t e = ensure_smem((const void*)k_nmf_mma<K, NBW, PERSIST>, (int)smem, attr);
+    constexpr int MTH = MWT * 32;
+    const size_t smem = mma_smem_bytes(NBW, K, MWT);
+    cudaError_t e = ensure_smem((const void*)k_nmf_mma<K, NBW, PERSIST, MWT>, (int)smem, attr);
     if (e != cudaSuccess) return e;
     MmaArgs A{};
     A.Yc = static_cast<const uint8_t*>(w.Yc);
@@ -731,13 +773,13 @@ cudaError_t mma_klb(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* 
     A.obj = obj;
     A.bar = bar;
     if (!PERSIST) {
-        k_nmf_mma<K, NBW, false><<<p.nblk_f, MTH, smem, s>>>(A);
+        k_nmf_mma<K, NBW, false, MWT><<<p.nblk_f, MTH, smem, s>>>(A);
         return cudaGetLastError();
     }
     e = cudaMemsetAsync(bar, 0, sizeof(unsigned), s);  // grid-barrier arrival counter
     if (e != cudaSuccess) return e;
     void* args[] = {&A};
-    return cudaLaunchCooperativeKernel((const void*)k_nmf_mma<K, NBW, true>, dim3(p.nblk_f), dim3(MTH), args, smem,
+    return cudaLaunchCooperativeKernel((const void*)k_nmf_mma<K, NBW, true, MWT>, dim3(p.nblk_f), dim3(MTH), args, smem,
                                        s);
 }
 
@@ -759,6 +801,19 @@ cudaError_t mma_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, fl
     }
 }
 
+// K = 9..16 on 16 warps (plan.mma_MW = 16; instantiated in nmf_mma_hi16.cu): <= 5 blocks per warp
+template <int K, bool PERSIST>
+cudaError_t mma_launch_k16(const Geometry& g, const NmfPlan& p, const NmfWs& w, float* V, float* D, int it,
+                           int n_iter, double* obj, unsigned* bar, unsigned* status, cudaStream_t s) {
+    switch (p.mma_NBW) {
+#define C(NB) \
+    case NB: return mma_klb<K, NB, PERSIST, MW16>(g, p, w, V, D, it, n_iter, obj, bar, status, s);
+        C(1) C(2) C(3) C(4) C(5)
+#undef C
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 #define HSNCT_MMA_EXTERN(KV)                                                                                  \
     extern template cudaError_t mma_launch_k<KV, false>(const Geometry&, const NmfPlan&, const NmfWs&, float*,  \
                                                         float*, int, int, double*, unsigned*, unsigned*,         \
@@ -766,6 +821,15 @@ cudaError_t mma_launch_k(const Geometry& g, const NmfPlan& p, const NmfWs& w, fl
     extern template cudaError_t mma_launch_k<KV, true>(const Geometry&, const NmfPlan&, const NmfWs&, float*,   \
                                                        float*, int, int, double*, unsigned*, unsigned*,          \
                                                        cudaStream_t);
+#define HSNCT_MMA16_EXTERN(KV)                                                                                \
+    extern template cudaError_t mma_launch_k16<KV, false>(const Geometry&, const NmfPlan&, const NmfWs&, float*, \
+                                                          float*, int, int, double*, unsigned*, unsigned*,       \
+                                                          cudaStream_t);                                         \
+    extern template cudaError_t mma_launch_k16<KV, true>(const Geometry&, const NmfPlan&, const NmfWs&, float*,  \
+                                                         float*, int, int, double*, unsigned*, unsigned*,        \
+                                                         cudaStream_t);
+#define HSNCT_MMA_KHI(M) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
+HSNCT_MMA_KHI(HSNCT_MMA16_EXTERN)
 #define HSNCT_MMA_K(M) M(1) M(2) M(3) M(4) M(5) M(6) M(7) M(8) M(9) M(10) M(11) M(12) M(13) M(14) M(15) M(16)
 HSNCT_MMA_K(HSNCT_MMA_EXTERN)
 

@@ -33,7 +33,9 @@ def main():
     res = {}
     for plan in plans:
         # "tcre": the tcgen05 pass with phase 2 re-streaming its chunks from L2
-        os.environ["HSNCT_NMF"] = "tc" if plan.startswith("tc") else plan
+        # "mma16": K = 9..16 on the 16-warp form of the mma pass (default: 8 warps)
+        os.environ["HSNCT_NMF"] = "tc" if plan.startswith("tc") else "mma" if plan.startswith("mma") else plan
+        os.environ["HSNCT_MMA_MW"] = "16" if plan == "mma16" else "0"
         os.environ["HSNCT_TC_RESTREAM"] = "1" if plan == "tcre" else "0"
         h = Hsnct(cfg.Nv, cfg.Nr, cfg.Nc, cfg.Nk, cfg.K, device=0)
         V, D = V0.clone(), D0.clone()

@@ -224,3 +224,27 @@ def test_mma_degenerate_shapes(mm, Nc, Nv, Nr, Nk, K):
     h.sync()
     Vo, Do = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), 8)
     assert rel(V, Vo) <= 1e-4 and rel(D, Do) <= 1e-4, (rel(V, Vo), rel(D, Do))
+
+
+@pytest.mark.parametrize("cfg,n_iter", [c for c in CASES if c[0].K > 8] +
+                         [(sd.custom(idx=79, Nc=5, Nv=3, Nr=1, Nk=33, K=9, M=2), 8)])
+def test_mma_sixteen_warps(monkeypatch, mm, cfg, n_iter):
+    """K = 9..16 on the opt-in 16-warp form (HSNCT_MMA_MW=16: <= 5 blocks per warp, the half-warps
+    of the V update summing warps 0-7 and 8-15's partials): same parity bar, and the result agrees
+    with the default 8-warp form to fp32 summation order."""
+    pr = sd.make_problem(cfg)
+    out = []
+    for mw in ("16", "8"):
+        monkeypatch.setenv("HSNCT_MMA_MW", mw)
+        h = mm(cfg)
+        assert ("MW=16" in h.debug_plan()) == (mw == "16"), h.debug_plan()
+        V = pr["V0"].to(DEV).clone()
+        D = pr["D0"].to(DEV).clone()
+        h.subspace_decompose(padded(pr["Y"], ((cfg.Nk + 3) // 4) * 4 + 4), V, D, n_iter)
+        h.sync()
+        h.close()
+        out.append((V, D))
+    Vo, Do = oracle.nmf(pr["Y"].numpy(), pr["V0"].numpy(), pr["D0"].numpy(), n_iter)
+    for V, D in out:
+        assert rel(V, Vo) <= 1e-3 and rel(D, Do) <= 1e-3, (rel(V, Vo), rel(D, Do))
+    assert rel(out[0][0], out[1][0].cpu().double().numpy()) <= 1e-4
