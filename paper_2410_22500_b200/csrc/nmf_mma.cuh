@@ -163,6 +163,12 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
     constexpr bool DISTV = true;
 #endif
     static_assert(DISTV || MWT == 8, "16 warps: the per-tile V update only");
+    // PK (K = 9..12): the second column block carries components 8..11 as interleaved hi/lo
+    // column pairs (column 2i: hi of component 8 + i, column 2i + 1: lo), so one MMA gives the
+    // hi.hi and hi.lo products and a second one lo.hi (+ lo.lo): 5 MMAs per block and phase
+    // instead of 6, half the second block's accumulators and D-operand registers.  Lane (g, t)
+    // then holds component 8 + t of that block (the two columns' sum), rows / bins g and g + 8.
+    constexpr bool PK = DISTV && NC == 2 && K <= 12;
     constexpr int KK = K * K;
     constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [2 NC values][NC column blocks][32 lanes]
     extern __shared__ __align__(128) uint8_t smem[];
@@ -178,6 +184,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
     // exponents of the per-component scales sigma_V (zero for components >= K)
     __shared__ __align__(16) uint32_t vfrag_s[DISTV ? 8 * NC * 16 : 4];
     __shared__ __align__(8) int ev_s[DISTV ? 8 * NC : 2];
+    __shared__ __align__(8) uint32_t vpk_s[PK ? 64 : 2];  // PK: packed block [column][t][b0, b1]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
     const int c = blockIdx.x, nC = gridDim.x;
     const size_t slotb = (size_t)NBW * BLK;
@@ -232,6 +239,8 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
     if constexpr (DISTV) {
         for (int i = tid; i < 8 * NC * 16; i += MTH) vfrag_s[i] = 0u;
         for (int i = tid; i < 8 * NC; i += MTH) ev_s[i] = 0;
+        if constexpr (PK)
+            for (int i = tid; i < 64; i += MTH) vpk_s[i] = 0u;
     }
 
     // D update slice of this CTA (PERSIST)
@@ -267,7 +276,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
         float invA[NC][2];  // 1 / sigma_D[k] for this lane's output columns k = 2t, 2t + 1 (+ 8 nc)
 #pragma unroll
         for (int nc = 0; nc < NC; ++nc) {
-            const int kd = g + 8 * nc;
+            const int kd = (PK && nc == 1) ? 8 + (g >> 1) : g + 8 * nc;
             float dv[NBW][4];
             float mx = 0.f;
 #pragma unroll
@@ -286,6 +295,10 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             for (int j = 0; j < NBW; ++j) {
                 dh[j][nc][0] = split2(dv[j][0] * sd, dv[j][1] * sd, dl[j][nc][0]);
                 dh[j][nc][1] = split2(dv[j][2] * sd, dv[j][3] * sd, dl[j][nc][1]);
+                if (PK && nc == 1 && (g & 1)) {  // odd column: the lo part (dl of the block is unused)
+                    dh[j][nc][0] = dl[j][nc][0];
+                    dh[j][nc][1] = dl[j][nc][1];
+                }
             }
             invA[nc][0] = pow2(-__shfl_sync(0xffffffffu, ed, 8 * t));  // (x 1 / sigma_Y of the tile)
             invA[nc][1] = pow2(-__shfl_sync(0xffffffffu, ed, 8 * t + 4));
@@ -331,6 +344,11 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                     ldsm4(yl, ba + 512 + lane * 16);
 #pragma unroll
                     for (int nc = 0; nc < NC; ++nc) {
+                        if (PK && nc == 1) {  // columns (hi, lo) of components 8..11
+                            mma16816(a0[nc], yh, dh[j][nc][0], dh[j][nc][1]);
+                            mma16816(a1[nc], yl, dh[j][nc][0], dh[j][nc][1]);
+                            continue;
+                        }
                         mma16816(a0[nc], yh, dh[j][nc][0], dh[j][nc][1]);
                         mma16816(a1[nc], yh, dl[j][nc][0], dl[j][nc][1]);
                         // (NC = 2: both small products in one accumulator, for the registers)
@@ -342,6 +360,13 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             for (int nc = 0; nc < NC; ++nc) {
                 float* rb = red + (size_t)(((n & (NRB - 1)) * MW + warp) * NC + nc) * 128;
                 const float i0 = invA[nc][0] * isy, i1 = invA[nc][1] * isy;
+                if (PK && nc == 1) {
+                    // component kk = t of the block, rows g and g + 8: the reader's slot of (kk, row)
+                    const int wp = (((4 * t + (g >> 1)) ^ (t >> 1)) << 2) + (g & 1);
+                    rb[wp] = ((a0[nc][0] + a0[nc][1]) + (a1[nc][0] + a1[nc][1])) * i0;
+                    rb[wp + 2] = ((a0[nc][2] + a0[nc][3]) + (a1[nc][2] + a1[nc][3])) * i0;
+                    continue;
+                }
                 rb[wo0] = (a0[nc][0] + (a1[nc][0] + a2[nc][0])) * i0;
                 rb[wo1] = (a0[nc][1] + (a1[nc][1] + a2[nc][1])) * i1;
                 rb[wo0 + 2] = (a0[nc][2] + (a1[nc][2] + a2[nc][2])) * i0;
@@ -428,6 +453,14 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                         fr[0] = hh;
                         fr[4] = hl;
                         if (r == 0) ev_s[k] = ev;
+                        if constexpr (PK) {
+                            if (k >= 8) {  // packed block: column 2 (k - 8) hi, 2 (k - 8) + 1 lo
+                                __half* fp = reinterpret_cast<__half*>(vpk_s) +
+                                             (((2 * (k - 8)) * 4 + u) * 2 + (r >> 3)) * 2 + (r & 1);
+                                fp[0] = hh;
+                                fp[16] = hl;
+                            }
+                        }
                     }
                     if (r < nv && (MW == 8 || lane < 16)) {
                         if (first && !(isfinite(v0) && v0 >= 0.f)) bad |= ST_INIT_BAD;
@@ -440,7 +473,14 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             }
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
-              if constexpr (DISTV) {
+              if (PK && nc == 1) {
+                // packed block: this lane's column g (hi or lo of component 8 + g / 2); the outputs
+                // (columns 2t, 2t + 1) belong to component 8 + t
+                const uint2 f = *reinterpret_cast<const uint2*>(&vpk_s[lane * 2]);
+                vh0[nc] = f.x;
+                vh1[nc] = f.y;
+                invB[nc][0] = isy * pow2(-ev_s[8 + t]);
+              } else if constexpr (DISTV) {
                 const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(8 * nc * 4 + lane) * 4]);
                 vh0[nc] = f.x;
                 vh1[nc] = f.y;
@@ -506,6 +546,20 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                         }
                     }
                 if constexpr (!DISTV) vdotA += (double)va;
+                uint32_t vp0 = 0u, vp1 = 0u;
+                if constexpr (PK) {  // H needs block 1 component-per-column: the unpacked fragments
+                    vp0 = vh0[1];
+                    vp1 = vh1[1];
+                    const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(8 * 4 + lane) * 4]);
+                    vh0[1] = f.x;
+                    vh1[1] = f.y;
+                    vl0[1] = f.z;
+                    vl1[1] = f.w;
+                    evs[1] = ev_s[g + 8];
+                    const int2 e2 = *reinterpret_cast<const int2*>(&ev_s[2 * t + 8]);
+                    ivB[1][0] = pow2(-e2.x);
+                    ivB[1][1] = pow2(-e2.y);
+                }
                 // H on the tensor core: A operand V^T (rows g, g + 8: this lane's B-operand
                 // fragments of column blocks 0 and 1), B operand V (column block nb2):
                 // C[g (+8)][2t + i + 8 nb2] = sum_r V[r][.] V[r][.], scaled by sigma_V sigma_V
@@ -524,6 +578,10 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                         hd += (double)(hc[q] * (ir * ivB[nb2][q & 1]));
                     }
                 }
+                if constexpr (PK) {  // back to the packed block for phase 2
+                    vh0[1] = vp0;
+                    vh1[1] = vp1;
+                }
             }
             // ---- phase 2: B^T[l][k] += sum_r Y+[r][l] V_new[r][k] over this warp's blocks (blocks
             //      j >= nb accumulate a copy of the last block into columns that are never stored)
@@ -537,6 +595,13 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
 #pragma unroll
                     for (int nc = 0; nc < NC; ++nc) {
                         float cc[4] = {0.f, 0.f, 0.f, 0.f};
+                        if (PK && nc == 1) {  // bins g, g + 8 of component 8 + t: hi and lo columns summed
+                            mma16816(cc, th, vh0[nc], vh1[nc]);
+                            mma16816(cc, tl, vh0[nc], vh1[nc]);
+                            bacc[j][nc][0] = fmaf(cc[0] + cc[1], invB[nc][0], bacc[j][nc][0]);
+                            bacc[j][nc][2] = fmaf(cc[2] + cc[3], invB[nc][0], bacc[j][nc][2]);
+                            continue;
+                        }
                         mma16816(cc, th, vh0[nc], vh1[nc]);
                         mma16816(cc, th, vl0[nc], vl1[nc]);
                         mma16816(cc, tl, vh0[nc], vh1[nc]);
@@ -571,6 +636,13 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                 const int l = 16 * (jb + j) + g;
 #pragma unroll
                 for (int nc = 0; nc < NC; ++nc) {
+                    if (PK && nc == 1) {
+                        if (8 + t < K) {
+                            if (l < A.Nk) Bo[(int64_t)(8 + t) * A.Nkp + l] = bacc[j][nc][0];
+                            if (l + 8 < A.Nk) Bo[(int64_t)(8 + t) * A.Nkp + l + 8] = bacc[j][nc][2];
+                        }
+                        continue;
+                    }
                     const int k0 = 2 * t + 8 * nc;
                     if (k0 < K) {
                         if (l < A.Nk) Bo[(int64_t)k0 * A.Nkp + l] = bacc[j][nc][0];
