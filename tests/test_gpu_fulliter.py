@@ -56,6 +56,9 @@ CASES = [
     pytest.param(sd.reduced(sd.CONFIGS[3], 2), sd.CONFIGS[3], id="C3r-200it"),
     pytest.param(sd.reduced(sd.CONFIGS[4], 2), sd.CONFIGS[4], id="C4r-300it"),
     pytest.param(sd.reduced(sd.CONFIGS[5], 2), sd.CONFIGS[5], id="C5r-300it"),
+    # the paper's Table I shape (K = 9: the packed second column block of the mma pass); four
+    # slices, so that the reduced problem has the 60K rows from which the mma plan is the default
+    pytest.param(sd.reduced(sd.CONFIGS[6], 4), sd.CONFIGS[6], id="C6r-300it"),
 ]
 
 
