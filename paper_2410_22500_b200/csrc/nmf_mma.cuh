@@ -28,7 +28,9 @@
 // Precision (R20): the same fp16 hi/lo split as the tcgen05 pass: x = (hi + lo)/s,
 // |error| <= 2^-22 |x| in the normal range, power-of-two scales s with s max < 2^14 -- one per
 // 16-row tile for Y+ (k_mma_prep), one per component and warp (bin range) for D, one per
-// component and tile for V.  Three MMAs per block (hi.hi + hi.lo + lo.hi; lo.lo is below 2^-22).  Phase-1
+// component and tile for V.  Three MMAs per block (hi.hi + hi.lo + lo.hi; lo.lo is below 2^-22);
+// a column block with <= 4 components (K <= 4; the second block at K = 9..12) is packed as
+// interleaved hi/lo columns and takes two (PK below).  Phase-1
 // accumulators run over one warp's 13 blocks; phase-2 accumulators cover one block of one tile
 // and are added to the fp32 register sums with their scale (FFMA), so no tensor-core sum is
 // longer than 39 MMAs.  Cross-warp and cross-CTA sums are fp32 / fp64 in a fixed order:
@@ -163,12 +165,15 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
     constexpr bool DISTV = true;
 #endif
     static_assert(DISTV || MWT == 8, "16 warps: the per-tile V update only");
-    // PK (K = 9..12): the second column block carries components 8..11 as interleaved hi/lo
+    // PK (K = 1..4 and 9..12): the last column block (PB) holds at most four components and
+    // carries them -- PK0 = 8 PB onwards; below for K = 9..12 -- as interleaved hi/lo
     // column pairs (column 2i: hi of component 8 + i, column 2i + 1: lo), so one MMA gives the
     // hi.hi and hi.lo products and a second one lo.hi (+ lo.lo): 5 MMAs per block and phase
     // instead of 6, half the second block's accumulators and D-operand registers.  Lane (g, t)
     // then holds component 8 + t of that block (the two columns' sum), rows / bins g and g + 8.
-    constexpr bool PK = DISTV && NC == 2 && K <= 12;
+    // (K <= 4: 2 MMAs per block and phase instead of 3.)
+    constexpr int PB = NC - 1, PK0 = 8 * PB;
+    constexpr bool PK = DISTV && K - PK0 <= 4;
     constexpr int KK = K * K;
     constexpr int HW = 64 * NC * NC;  // per-warp H accumulators [2 NC values][NC column blocks][32 lanes]
     extern __shared__ __align__(128) uint8_t smem[];
@@ -276,7 +281,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
         float invA[NC][2];  // 1 / sigma_D[k] for this lane's output columns k = 2t, 2t + 1 (+ 8 nc)
 #pragma unroll
         for (int nc = 0; nc < NC; ++nc) {
-            const int kd = (PK && nc == 1) ? 8 + (g >> 1) : g + 8 * nc;
+            const int kd = (PK && nc == PB) ? PK0 + (g >> 1) : g + 8 * nc;
             float dv[NBW][4];
             float mx = 0.f;
 #pragma unroll
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             for (int j = 0; j < NBW; ++j) {
                 dh[j][nc][0] = split2(dv[j][0] * sd, dv[j][1] * sd, dl[j][nc][0]);
                 dh[j][nc][1] = split2(dv[j][2] * sd, dv[j][3] * sd, dl[j][nc][1]);
-                if (PK && nc == 1 && (g & 1)) {  // odd column: the lo part (dl of the block is unused)
+                if (PK && nc == PB && (g & 1)) {  // odd column: the lo part (dl of the block is unused)
                     dh[j][nc][0] = dl[j][nc][0];
                     dh[j][nc][1] = dl[j][nc][1];
                 }
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                     ldsm4(yl, ba + 512 + lane * 16);
 #pragma unroll
                     for (int nc = 0; nc < NC; ++nc) {
-                        if (PK && nc == 1) {  // columns (hi, lo) of components 8..11
+                        if (PK && nc == PB) {  // columns (hi, lo) of components PK0..PK0 + 3
                             mma16816(a0[nc], yh, dh[j][nc][0], dh[j][nc][1]);
                             mma16816(a1[nc], yl, dh[j][nc][0], dh[j][nc][1]);
                             continue;
@@ -360,7 +365,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             for (int nc = 0; nc < NC; ++nc) {
                 float* rb = red + (size_t)(((n & (NRB - 1)) * MW + warp) * NC + nc) * 128;
                 const float i0 = invA[nc][0] * isy, i1 = invA[nc][1] * isy;
-                if (PK && nc == 1) {
+                if (PK && nc == PB) {
                     // component kk = t of the block, rows g and g + 8: the reader's slot of (kk, row)
                     const int wp = (((4 * t + (g >> 1)) ^ (t >> 1)) << 2) + (g & 1);
                     rb[wp] = ((a0[nc][0] + a0[nc][1]) + (a1[nc][0] + a1[nc][1])) * i0;
@@ -454,9 +459,9 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                         fr[4] = hl;
                         if (r == 0) ev_s[k] = ev;
                         if constexpr (PK) {
-                            if (k >= 8) {  // packed block: column 2 (k - 8) hi, 2 (k - 8) + 1 lo
+                            if (k >= PK0) {  // packed block: column 2 (k - PK0) hi, 2 (k - PK0) + 1 lo
                                 __half* fp = reinterpret_cast<__half*>(vpk_s) +
-                                             (((2 * (k - 8)) * 4 + u) * 2 + (r >> 3)) * 2 + (r & 1);
+                                             (((2 * (k - PK0)) * 4 + u) * 2 + (r >> 3)) * 2 + (r & 1);
                                 fp[0] = hh;
                                 fp[16] = hl;
                             }
@@ -473,13 +478,13 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
             }
 #pragma unroll
             for (int nc = 0; nc < NC; ++nc) {
-              if (PK && nc == 1) {
-                // packed block: this lane's column g (hi or lo of component 8 + g / 2); the outputs
-                // (columns 2t, 2t + 1) belong to component 8 + t
+              if (PK && nc == PB) {
+                // packed block: this lane's column g (hi or lo of component PK0 + g / 2); the outputs
+                // (columns 2t, 2t + 1) belong to component PK0 + t
                 const uint2 f = *reinterpret_cast<const uint2*>(&vpk_s[lane * 2]);
                 vh0[nc] = f.x;
                 vh1[nc] = f.y;
-                invB[nc][0] = isy * pow2(-ev_s[8 + t]);
+                invB[nc][0] = isy * pow2(-ev_s[PK0 + t]);
               } else if constexpr (DISTV) {
                 const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(8 * nc * 4 + lane) * 4]);
                 vh0[nc] = f.x;
@@ -547,18 +552,18 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                     }
                 if constexpr (!DISTV) vdotA += (double)va;
                 uint32_t vp0 = 0u, vp1 = 0u;
-                if constexpr (PK) {  // H needs block 1 component-per-column: the unpacked fragments
-                    vp0 = vh0[1];
-                    vp1 = vh1[1];
-                    const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(8 * 4 + lane) * 4]);
-                    vh0[1] = f.x;
-                    vh1[1] = f.y;
-                    vl0[1] = f.z;
-                    vl1[1] = f.w;
-                    evs[1] = ev_s[g + 8];
-                    const int2 e2 = *reinterpret_cast<const int2*>(&ev_s[2 * t + 8]);
-                    ivB[1][0] = pow2(-e2.x);
-                    ivB[1][1] = pow2(-e2.y);
+                if constexpr (PK) {  // H needs block PB component-per-column: the unpacked fragments
+                    vp0 = vh0[PB];
+                    vp1 = vh1[PB];
+                    const uint4 f = *reinterpret_cast<const uint4*>(&vfrag_s[(PK0 * 4 + lane) * 4]);
+                    vh0[PB] = f.x;
+                    vh1[PB] = f.y;
+                    vl0[PB] = f.z;
+                    vl1[PB] = f.w;
+                    evs[PB] = ev_s[g + PK0];
+                    const int2 e2 = *reinterpret_cast<const int2*>(&ev_s[2 * t + PK0]);
+                    ivB[PB][0] = pow2(-e2.x);
+                    ivB[PB][1] = pow2(-e2.y);
                 }
                 // H on the tensor core: A operand V^T (rows g, g + 8: this lane's B-operand
                 // fragments of column blocks 0 and 1), B operand V (column block nb2):
@@ -579,8 +584,8 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                     }
                 }
                 if constexpr (PK) {  // back to the packed block for phase 2
-                    vh0[1] = vp0;
-                    vh1[1] = vp1;
+                    vh0[PB] = vp0;
+                    vh1[PB] = vp1;
                 }
             }
             // ---- phase 2: B^T[l][k] += sum_r Y+[r][l] V_new[r][k] over this warp's blocks (blocks
@@ -595,7 +600,7 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
 #pragma unroll
                     for (int nc = 0; nc < NC; ++nc) {
                         float cc[4] = {0.f, 0.f, 0.f, 0.f};
-                        if (PK && nc == 1) {  // bins g, g + 8 of component 8 + t: hi and lo columns summed
+                        if (PK && nc == PB) {  // bins g, g + 8 of component PK0 + t: hi and lo columns summed
                             mma16816(cc, th, vh0[nc], vh1[nc]);
                             mma16816(cc, tl, vh0[nc], vh1[nc]);
                             bacc[j][nc][0] = fmaf(cc[0] + cc[1], invB[nc][0], bacc[j][nc][0]);
@@ -636,10 +641,10 @@ __global__ void __launch_bounds__(MWT * 32, 1) k_nmf_mma(MmaArgs A) {
                 const int l = 16 * (jb + j) + g;
 #pragma unroll
                 for (int nc = 0; nc < NC; ++nc) {
-                    if (PK && nc == 1) {
-                        if (8 + t < K) {
-                            if (l < A.Nk) Bo[(int64_t)(8 + t) * A.Nkp + l] = bacc[j][nc][0];
-                            if (l + 8 < A.Nk) Bo[(int64_t)(8 + t) * A.Nkp + l + 8] = bacc[j][nc][2];
+                    if (PK && nc == PB) {
+                        if (PK0 + t < K) {
+                            if (l < A.Nk) Bo[(int64_t)(PK0 + t) * A.Nkp + l] = bacc[j][nc][0];
+                            if (l + 8 < A.Nk) Bo[(int64_t)(PK0 + t) * A.Nkp + l + 8] = bacc[j][nc][2];
                         }
                         continue;
                     }
