@@ -589,7 +589,26 @@ def run_hsnct(args, cfg, n_iter, rank, world, local_rank):
     # copy of ALL of x^h (window by window into a two-window host ring, overlapped with the
     # synthesis of the next window) plus V and D
     e2e = None
-    if not args.no_e2e:
+    e2e_ok = not args.no_e2e
+    if e2e_ok:
+        # host memory for the pinned copy of Y (and the counts, the ring): every local rank holds
+        # its own; skip the end-to-end leg rather than drive the box out of memory
+        try:
+            import psutil
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+            need = 1.25 * Y.numel() * Y.element_size() + (4 << 30)
+            avail = psutil.virtual_memory().available / max(1, local_world)
+            if need > 0.9 * avail:
+                e2e_ok = False
+                sys.stderr.write(f"[bench] e2e skipped: needs {need / 2**30:.0f} GiB of host memory per rank, "
+                                 f"{avail / 2**30:.0f} GiB available\n")
+        except ImportError:
+            pass
+        if world > 1:  # one decision for all ranks (the leg has barriers)
+            flag = torch.tensor([1 if e2e_ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            e2e_ok = bool(flag.item())
+    if e2e_ok:
         Yh = Y.cpu().pin_memory()
         V0h, D0h = V0.cpu().pin_memory(), D0.cpu().pin_memory()
         del Y, Xh, ws_nmf, ws_fbp
