@@ -18,7 +18,7 @@ INC = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libhsnct.so")
 BUILD = os.path.join(HERE, "build")
 
-SOURCES = (["api.cpp", "nmf.cu", "nmf_fused.cu", "nmf_tc.cu", "nmf_mma.cu", "nmf_mma_lo.cu", "nmf_mma_hi.cu", "nmf_mma_hi16.cu", "fbp.cu", "synth.cu", "fmd.cu", "mbir.cu", "counts.cu"]
+SOURCES = (["api.cpp", "nmf.cu", "nmf_fused.cu", "nmf_tc.cu", "nmf_mma.cu", "nmf_mma_lo.cu", "nmf_mma_hi.cu", "fbp.cu", "synth.cu", "fmd.cu", "mbir.cu", "counts.cu"]
            + [f"nmf_fused_k{k}.cu" for k in range(1, 17)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++20", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -50,7 +50,10 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False, var
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(INC, "hsnct.h"))
     cmds, objs = [], []
-    for src in SOURCES:
+    # the 16-warp K > 8 form of the mma pass (measured slower) is compiled only into
+    # an experimental variant: build.py --variant=mw16 -DHSNCT_MMA_MW16
+    sources = SOURCES + (["nmf_mma_hi16.cu"] if "HSNCT_MMA_MW16" in defines else [])
+    for src in sources:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)

@@ -193,15 +193,17 @@ int nbw_of(int NB, int mw) {
 bool nmf_mma_plan(const Geometry& g, int num_sms, NmfPlan* p) {
     if (g.K > 16) return false;
     const int NB = (g.Nk + 15) / 16;
-    // K = 9..16 (two column blocks): 8 warps with <= 10 blocks each (255 registers); HSNCT_MMA_MW=16
-    // selects the 16-warp form (<= 5 blocks per warp, 128 registers, four warps per scheduler),
+    // K = 9..16 (two column blocks): 8 warps with <= 10 blocks each (255 registers).  In a build with
+    // -DHSNCT_MMA_MW16 (not the product library), HSNCT_MMA_MW=16 selects the 16-warp form (<= 5 blocks per warp, 128 registers, four warps per scheduler),
     // measured slower at C6 (12.1 vs 10.4 ms per iteration: the per-warp, per-tile work -- partial-A
     // exchange, operand loads, barriers -- is paid 16 times; profiles/r02/session4/ab_split.txt)
     int mw = MW;
+#ifdef HSNCT_MMA_MW16  // experimental build only (build.py --variant=mw16 -DHSNCT_MMA_MW16)
     if (g.K > 8) {
         const char* e = getenv("HSNCT_MMA_MW");
         if (e && atoi(e) == 16) mw = MW16;
     }
+#endif
     const int nbw = nbw_of(NB, mw);
     if (!nbw) return false;
     if (g.K > 8 && nbw > 10) return false;  // two column blocks: registers for <= 10 blocks per warp
@@ -256,12 +258,14 @@ cudaError_t nmf_mma_launch(const Geometry& g, const NmfPlan& p, const NmfWs& w, 
     case KV: return mma_launch_k<KV, false>(g, p, w, V, const_cast<float*>(D), it, 1, nullptr, nullptr, status, s);
 #define M16(KV) \
     case KV: return mma_launch_k16<KV, false>(g, p, w, V, const_cast<float*>(D), it, 1, nullptr, nullptr, status, s);
+#ifdef HSNCT_MMA_MW16
     if (p.mma_MW == MW16) {
         switch (g.K) {
             HSNCT_MMA_KHI(M16)
             default: return cudaErrorInvalidValue;
         }
     }
+#endif
     switch (g.K) {
         HSNCT_MMA_K(M)
         default: return cudaErrorInvalidValue;
@@ -276,12 +280,14 @@ cudaError_t nmf_mma_persist_launch(const Geometry& g, const NmfPlan& p, const Nm
     case KV: return mma_launch_k<KV, true>(g, p, w, V, D, 0, n_iter, obj, bar, status, s);
 #define M16(KV) \
     case KV: return mma_launch_k16<KV, true>(g, p, w, V, D, 0, n_iter, obj, bar, status, s);
+#ifdef HSNCT_MMA_MW16
     if (p.mma_MW == MW16) {
         switch (g.K) {
             HSNCT_MMA_KHI(M16)
             default: return cudaErrorInvalidValue;
         }
     }
+#endif
     switch (g.K) {
         HSNCT_MMA_K(M)
         default: return cudaErrorInvalidValue;
